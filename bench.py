@@ -1,0 +1,316 @@
+"""Benchmark: GMRES-IR solve time to 1e-10 on 3D Laplace 150^3 (BASELINE.json
+configs[1]; n = 3,375,000, nnz = 23,490,000), GMRES(50), b = ones, x0 = 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+One "step" = one complete GMRES-IR solve from x0 = 0 to rel. residual 1e-10
+(~2400 fp32 inner iterations).  The matrix, right-hand side and fp32 copy
+are resident in HBM before the timed region (the reference also excludes
+the fp32 copy, solvers.py:321); the working set (A64 + A32 + V32 ~ 1.2 GB)
+is ~10x the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  Extra keys: fp64 GMRES(50) solve time and
+the IR speedup on the same GPU, iteration counts, the per-kernel-class
+device time of one profiled cycle, the roofline of the dominant kernel,
+the CPU oracle timed on this host (cpu_baseline), and the end-to-end time
+through the public API with host (numpy) inputs (e2e).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMRES-IR solve time to 1e-10 rel residual; speedup vs fp64 GMRES; HBM GB/s"
+PUBLISHED_V100_IR_S = 11.75      # Laplace3D150 GMRES-IR on V100
+REFERENCE_IR_ITERS = 2400        # reference/paper iteration count at this config
+NX = 150
+M = 50
+RTOL = 1e-10
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int = 0):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic byte model
+
+def cycle_bytes(n: int, nnz: int, m: int, s: int) -> dict[str, float]:
+    """Algorithmic bytes per cycle for each fused kernel class, s = value size."""
+    spmv = nnz * (s + 4) + 4 * (n + 1) + 2 * n * s           # CSR + x once + y once
+    ks = range(1, m + 1)
+    return {
+        "spmv_dot1": sum(spmv + k * n * s for k in ks),       # + read V[0..k) for pass-1 dots
+        "update_dot": sum((k + 2) * n * s for k in ks),       # read V[0..k) + w, write w
+        "update_norm_givens": sum((k + 2) * n * s for k in ks),
+        "scale": m * 2 * n * s,
+    }
+
+
+def native_arm(args, rank: int, world: int):
+    import numpy as np
+    import torch
+
+    import paper_2109_01232_b200 as P
+    from paper_2109_01232_b200 import _lib
+    from paper_2109_01232_b200.core import FP32, FP64, convert_matrix, padded_copy, dvec
+    from paper_2109_01232_b200.solvers import NativeSolve, StopCriteria, gmres_ir
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    spec = P.StencilSpec(P.StencilKind.LAPLACE3D, NX)
+    A = P.generate(spec)
+    n, nnz = A.n_rows, A.nnz
+    b = torch.ones(n, dtype=torch.float64, device="cuda")
+    crit = StopCriteria(rtol=RTOL, m=M)
+    # warm-up (also builds + caches the CUDA graphs' kernels/attributes)
+    for _ in range(args.warmup):
+        rep = gmres_ir(A, b, criteria=crit)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    l0 = _lib.launch_count()
+    times, iters = [], []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(args.steps):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record()
+            if _ == 0:
+                e0.record()
+            rep = gmres_ir(A, b, criteria=crit)
+            s1.record()
+            s1.synchronize()
+            times.append(s0.elapsed_time(s1) / 1e3)
+            iters.append(rep.total_iters)
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    total_s = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([total_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_s = float(t.item())
+    solve_s = total_s / args.steps
+    x_ir = rep.x
+    res_ir, _ = P.explicit_residual(A, b, x_ir)
+    # fp64 GMRES(50) on the same GPU (speedup denominator)
+    t0 = time.perf_counter()
+    rep64 = P.gmres_restarted(A, b, criteria=crit)
+    torch.cuda.synchronize()
+    fp64_s = rep64.total_time
+    sol_diff = float(torch.linalg.norm(rep64.x - x_ir) / torch.linalg.norm(rep64.x))
+
+    # one profiled (eager) IR cycle: per-kernel-class device time
+    A32 = convert_matrix(A, FP32)
+    bd = padded_copy(b, FP64)
+    xd = dvec(n, FP64)
+    ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, bd, xd, M, RTOL)
+    ns.begin()
+    ns.cycle(M)                                   # warm
+    prof = ns.profile_cycle(M)
+    ns.close()
+    model = cycle_bytes(n, nnz, M, 4)
+    kernels = {}
+    for k, (ms, cnt) in prof.items():
+        kernels[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}
+        if k in model and ms > 0:
+            kernels[k]["GBps"] = round(model[k] / (ms / 1e3) / 1e9, 1)
+    peak, peak_kind = _peaks()
+    dom = max((k for k in model if k in prof), key=lambda k: prof[k][0])
+    dom_gbs = model[dom] / (prof[dom][0] / 1e3) / 1e9
+    cyc_ms = sum(v[0] for v in prof.values())
+    cyc_bytes = sum(model.values())
+
+    # end to end through the public API with HOST inputs (numpy CSR + b)
+    rp, ci, v = A.host_arrays()
+
+    class HostCsr:  # the reference's CsrMatrix shape (numpy arrays)
+        pass
+    Ah = HostCsr()
+    Ah.n_rows = Ah.n_cols = n
+    Ah.row_ptr, Ah.col_idx, Ah.values = rp, ci, v
+    bh = np.ones(n)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep_h = gmres_ir(Ah, bh, criteria=crit)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    h2d = rp.nbytes + ci.nbytes + v.nbytes + bh.nbytes
+    d2h = rep_h.x.nbytes
+
+    out = {
+        "metric": METRIC,
+        "value": round(solve_s, 5),
+        "unit": "s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(solve_s * 1e3, 3),
+        "higher_is_better": False,
+        "scaling": "replicas" if world > 1 else "strong",
+        "vs_baseline": round(solve_s / PUBLISHED_V100_IR_S, 5),
+        "vs_baseline_note": "value / published V100 GMRES-IR time 11.75 s (PAPER.md:461)",
+        "dtype": "f32 inner / f64 outer",
+        "data": "synthetic (reference generator, on device); b = ones, x0 = 0",
+        "config": {"workload": "gmres_ir laplace3d:150 GMRES(50) rtol=1e-10 (BASELINE configs[1])",
+                   "n": n, "nnz": nnz, "m": M, "rtol": RTOL,
+                   "l2": "working set ~1.2 GB >> 126 MB L2; no flush needed"},
+        "iters": iters[-1],
+        "iters_reference": REFERENCE_IR_ITERS,
+        "final_rel_residual": res_ir / float(torch.linalg.norm(b)),
+        "fp64_solve_s": round(fp64_s, 5),
+        "fp64_iters": rep64.total_iters,
+        "speedup_vs_fp64": round(fp64_s / solve_s, 3),
+        "solution_rel_diff_ir_vs_fp64": sol_diff,
+        "step_times_s": [round(t, 5) for t in times],
+        "profile_cycle": {"ms": round(cyc_ms, 4), "GBps_algorithmic": round(cyc_bytes / (cyc_ms / 1e3) / 1e9, 1),
+                          "kernels": kernels},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1), "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
+                     "traffic": None},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": {"value": round(e2e_s, 5), "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "iters": rep_h.total_iters},
+    }
+    return out
+
+
+def cpu_sample(threads: int | None):
+    """Oracle GMRES-IR at the bench config: one outer cycle (50 fp32 inner
+    iterations + the fp64 residual), extrapolated to the reference's 2400
+    iterations.  Returns (extrapolated_solve_s, sample_s)."""
+    import numpy as np
+    from oracle import cpu_gmres as O
+    A = O.stencil_csr("laplace3d", NX)
+    b = O.ones_rhs(A.n_rows)
+    t0 = time.perf_counter()
+    rep = O.solve_ir(A, b, m=M, max_iters=M, threads=threads)
+    dt = time.perf_counter() - t0
+    return dt / rep.total_iters * REFERENCE_IR_ITERS, dt
+
+
+def reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, _ = cpu_sample(threads)
+        if i >= args.warmup:
+            vals.append(v)
+    val = statistics.mean(vals)
+    return {
+        "metric": METRIC, "impl": "reference", "value": round(val, 3), "unit": "s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(val * 1e3, 1), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": round(val / PUBLISHED_V100_IR_S, 3), "dtype": "f32 inner / f64 outer",
+        "data": "synthetic; b = ones, x0 = 0",
+        "config": {"workload": "gmres_ir laplace3d:150 GMRES(50) rtol=1e-10 (BASELINE configs[1])"},
+        "cpu_baseline": {"value": round(val, 3), "unit": "s", "cores": threads, "kind": "port",
+                         "sample": "oracle/cpu_gmres.py solve_ir, one 50-iteration IR cycle per step "
+                                   "(+ fp64 residual), extrapolated x2400/50; BLAS threads = all host cores"},
+        "e2e": {"value": round(val, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        out = reference_arm(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        torch.distributed.init_process_group("nccl")
+    out = native_arm(args, rank, world)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            v, dt = cpu_sample(1)
+            out["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": 1, "kind": "port",
+                                   "sample": f"oracle solve_ir one 50-iteration IR cycle ({dt:.1f} s), "
+                                             "extrapolated x2400/50; 1 BLAS thread as the reference pins"}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,738 @@
+// CGS2 Arnoldi kernels (krylov.py:112-202, solvers.py:122-174).
+//
+// One Arnoldi step j (k = j + 1 basis vectors) is four launches:
+//   K_A  spmv_dot1     w = A z, ||w||, finite check, c1 = V^T w      (spmv_kernels.cu)
+//   K_B  update_dot    w <- w - V c1 ; c2 = V^T w ; H[:,j] = c1 + c2   (this file, TMA-staged)
+//   K_C  update_norm   w <- w - V c2 ; h_sub = ||w|| ; breakdown ;
+//                      Givens rotation ; implicit residual ; done flag (this file)
+//   K_S  step_scale    V[:, j+1] = w / h_sub                          (this file)
+// so the basis is swept three times per step (the reference's BLAS sequence
+// sweeps it four times).
+#include <algorithm>
+#include <mutex>
+
+#include "spmv.cuh"
+#include "state.cuh"
+
+namespace mpg {
+
+__device__ __forceinline__ bool gated(const mpg_state_header* h) {
+  return *(volatile const int*)&h->done != 0;
+}
+
+// ============================================================== K_B update_dot
+// TMA-staged: a producer warp bulk-copies the tile slices V[0..k)[tile] and
+// w[tile] into an S-stage shared ring; consumers form w' = w - V c1 from the
+// staged copy, then c2 partials = V^T w' from the same copy, so V is read
+// from HBM exactly once for both halves.
+
+constexpr int kUdConsumers = 256;
+constexpr int kUdThreads = kUdConsumers + 32;
+
+template <typename T>
+__global__ void __launch_bounds__(kUdThreads) k_update_dot(const T* __restrict__ V, long long ldv,
+                                                           long long n, int k, T* __restrict__ w,
+                                                           StateView<T> sv, WsView ws, int TB,
+                                                           int S) {
+  if (gated(sv.h)) return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  const size_t stage_elems = (size_t)(k + 1) * TB;
+  T* stages = reinterpret_cast<T*>(smraw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw + (size_t)S * stage_elems * sizeof(T));
+  uint64_t* empty = full + S;
+  T* c1s = reinterpret_cast<T*>(empty + S);
+  T* acc = c1s + k;
+  T* pw = acc + k;     // 8
+  T* red = pw + 8;     // 32
+  __shared__ bool lastflag;
+
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  const int nt = (int)((R1 - R0 + TB - 1) / TB);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kUdConsumers / 32);
+    }
+    fence_mbar_init();
+  }
+  for (int i = tid; i < k; i += blockDim.x) {
+    c1s[i] = sv.c1[i];
+    acc[i] = T(0);
+  }
+  __syncthreads();
+
+  if (warp == kUdConsumers / 32) {
+    if (lane == 0) {
+      for (int t = 0; t < nt; ++t) {
+        const int s = t % S;
+        if (t >= S) mbar_wait(&empty[s], ((t / S) - 1) & 1);
+        const long long a = R0 + (long long)t * TB;
+        const long long nr = min((long long)TB, R1 - a);
+        const uint32_t bytes = (uint32_t)round16(nr * (long long)sizeof(T));
+        T* dst = stages + (size_t)s * stage_elems;
+        fence_proxy_async();
+        mbar_expect_tx(&full[s], bytes * (uint32_t)(k + 1));
+        for (int i = 0; i < k; ++i) bulk_g2s(dst + (size_t)i * TB, V + (size_t)i * ldv + a, bytes, &full[s]);
+        bulk_g2s(dst + (size_t)k * TB, w + a, bytes, &full[s]);
+      }
+    }
+    return;
+  }
+
+  for (int t = 0; t < nt; ++t) {
+    const int s = t % S;
+    const long long a = R0 + (long long)t * TB;
+    const int nr = (int)min((long long)TB, R1 - a);
+    mbar_wait(&full[s], (t / S) & 1);
+    T* vs = stages + (size_t)s * stage_elems;
+    T* wsm = vs + (size_t)k * TB;
+    // phase 1: w' = w - V c1 (the second half of CGS pass 1, krylov.py:140)
+    for (int rr = tid; rr < nr; rr += kUdConsumers) {
+      T u = T(0);
+      int i = 0;
+      for (; i + 4 <= k; i += 4) {
+        u = fma_rn(vs[(size_t)(i + 0) * TB + rr], c1s[i + 0], u);
+        u = fma_rn(vs[(size_t)(i + 1) * TB + rr], c1s[i + 1], u);
+        u = fma_rn(vs[(size_t)(i + 2) * TB + rr], c1s[i + 2], u);
+        u = fma_rn(vs[(size_t)(i + 3) * TB + rr], c1s[i + 3], u);
+      }
+      for (; i < k; ++i) u = fma_rn(vs[(size_t)i * TB + rr], c1s[i], u);
+      const T wv = sub_rn(wsm[rr], u);
+      wsm[rr] = wv;
+      w[a + rr] = wv;
+    }
+    consumer_sync();
+    // phase 2: c2 partials = V^T w' (CGS pass 2 dot, krylov.py:139)
+    auto vrow = [&](int i) { return (const T*)(vs + (size_t)i * TB); };
+    tile_dots<T, kLoadShared>(k, nr, vrow, wsm, acc, pw);
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+  }
+  consumer_sync();
+  T* part = static_cast<T*>(ws.part);
+  for (int i = tid; i < k; i += kUdConsumers) part[(size_t)blockIdx.x * k + i] = acc[i];
+  (void)red;
+  __threadfence();
+  consumer_sync();
+  if (tid == 0) lastflag = (atomicAdd(ws.counter, 1u) == gridDim.x - 1);
+  consumer_sync();
+  if (lastflag) {
+    __threadfence();
+    if (tid == 0) *ws.counter = 0u;
+    const int j = k - 1;
+    for (int c = warp; c < k; c += kUdConsumers / 32) {
+      T s2 = T(0);
+      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        sv.c2[c] = s2;
+        // h = 0; h += c1; h += c2  (krylov.py:137-141)
+        sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);
+      }
+    }
+  }
+}
+
+// ================================== generic-operator pass-1 dots (no SpMV)
+// c1 = V[:, :k]^T w, w0 = ||w||, finite check (krylov.py:133-139) for a w
+// produced by an arbitrary operator.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_dot1_w(const T* __restrict__ w, long long n,
+                                                     const T* __restrict__ V, long long ldv, int k,
+                                                     StateView<T> sv, WsView ws) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  __shared__ T red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  const int stride = k + 2;
+  T* part = static_cast<T*>(ws.part);
+  const long long nv = (R1 - R0) / VN;
+  for (int i = warp; i < k; i += kWarps) {
+    const T* v = V + (size_t)i * ldv;
+    T p = T(0);
+    for (long long g = lane; g < nv; g += 32) {
+      T a[VN], b[VN];
+      vload_cs(v + R0 + g * VN, a);
+      vload(w + R0 + g * VN, b);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) p = fma_rn(a[e], b[e], p);
+    }
+    for (long long r = R0 + nv * VN + lane; r < R1; r += 32) p = fma_rn(v[r], w[r], p);
+    p = warp_sum(p);
+    if (lane == 0) part[(size_t)blockIdx.x * stride + i] = p;
+  }
+  T ss = T(0);
+  int bad = 0;
+  for (long long r = R0 + threadIdx.x; r < R1; r += kThreads) {
+    const T y = w[r];
+    ss = fma_rn(y, y, ss);
+    bad |= !isfinite(y);
+  }
+  const T t = block_sum(ss, red);
+  const int anybad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    part[(size_t)blockIdx.x * stride + k] = t;
+    part[(size_t)blockIdx.x * stride + k + 1] = anybad ? T(1) : T(0);
+  }
+  if (last_cta(ws.counter)) {
+    finalize_columns(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+      if (c < k) sv.c1[c] = s;
+      else if (c == k) sv.h->w0 = (double)sqrt_rn(s);
+      else if (s != T(0)) { sv.h->flags |= MPG_FLAG_NONFINITE_OP; sv.h->done = 1; }
+    });
+  }
+}
+
+// ================================================= K_C update_norm + Givens
+
+// glibc-style hypot for the fp64 rotation (np.hypot -> libm hypot);
+// fp32 follows glibc hypotf: correctly rounded double evaluation.
+__device__ __forceinline__ float hypot_ref(float a, float b) {
+  const double x = (double)a, y = (double)b;
+  return (float)__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+}
+__device__ double hypot_kernel(double ax, double ay) {
+  // ax >= ay > 0, both well inside the exponent range (Borges 2019, as glibc)
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    const double delta = h - ay;
+    t1 = ax * (ax - 2.0 * delta);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    const double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+__device__ __forceinline__ double hypot_ref(double a, double b) {
+  double ax = fabs(a), ay = fabs(b);
+  if (isinf(ax) || isinf(ay)) return __longlong_as_double(0x7ff0000000000000LL);
+  if (isnan(ax) || isnan(ay)) return ax + ay;
+  if (ax < ay) { const double t = ax; ax = ay; ay = t; }
+  if (ay == 0.0) return ax;
+  if (ax > 0x1p+511) {
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    return hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) * 0x1p+600;
+  }
+  if (ay < 0x1p-511) {
+    if (ax >= ay * 0x1p+54) return ax + ay;
+    return hypot_kernel(ax * 0x1p+600, ay * 0x1p+600) * 0x1p-600;
+  }
+  if (ay <= ax * 0x1p-54) return ax + ay;
+  return hypot_kernel(ax, ay);
+}
+
+// Rotate column j into the triangular factor (krylov.py:154-187).  One thread.
+template <typename T>
+__device__ void givens_column(const StateView<T>& sv, int j, double threshold, bool brk,
+                              int m_limit) {
+  T* col = &sv.Rc(j, 0);
+  for (int i = 0; i <= j + 1; ++i) col[i] = sv.Hc(j, i);
+  for (int i = 0; i < j; ++i) {
+    const T c = sv.cs[i], s = sv.sn[i];
+    const T a = col[i], b = col[i + 1];
+    const T top = add_rn(mul_rn(c, a), mul_rn(s, b));
+    col[i + 1] = add_rn(mul_rn(-s, a), mul_rn(c, b));
+    col[i] = top;
+  }
+  const T a = col[j], b = col[j + 1];
+  const T r = hypot_ref(a, b);
+  double res;
+  if (r == T(0)) {
+    sv.cs[j] = T(1);
+    sv.sn[j] = T(0);
+    res = (double)fabs(sv.g[j]);
+  } else {
+    const T c = div_rn(a, r), s = div_rn(b, r);
+    sv.cs[j] = c;
+    sv.sn[j] = s;
+    col[j] = add_rn(mul_rn(c, a), mul_rn(s, b));
+    col[j + 1] = T(0);
+    const T gj = sv.g[j], gj1 = sv.g[j + 1];
+    const T top = add_rn(mul_rn(c, gj), mul_rn(s, gj1));
+    sv.g[j + 1] = add_rn(mul_rn(-s, gj), mul_rn(c, gj1));
+    sv.g[j] = top;
+    res = (double)fabs(sv.g[j + 1]);
+  }
+  sv.implicit[j] = res;
+  sv.h->steps = j + 1;
+  sv.h->breakdown = brk ? 1 : 0;
+  // solvers.py:160-168: stop on breakdown, on the implicit threshold, or when
+  // the cycle's step budget is exhausted
+  if (brk || res <= threshold || j + 1 >= m_limit) sv.h->done = 1;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ V, long long ldv,
+                                                          long long n, int j, T* __restrict__ w,
+                                                          StateView<T> sv, WsView ws, int m_limit) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  const int k = j + 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  T* c2s = reinterpret_cast<T*>(smraw);
+  __shared__ T red[32];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) c2s[i] = sv.c2[i];
+  __syncthreads();
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  T ss = T(0);
+  const long long nv = (R1 - R0) / VN;
+  for (long long g = threadIdx.x; g < nv; g += kThreads) {
+    const long long r = R0 + g * VN;
+    T wv[VN], u[VN];
+    vload(w + r, wv);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) u[e] = T(0);
+    int i = 0;
+    for (; i + 4 <= k; i += 4) {
+      T v0[VN], v1[VN], v2[VN], v3[VN];
+      vload_cs(V + (size_t)(i + 0) * ldv + r, v0);
+      vload_cs(V + (size_t)(i + 1) * ldv + r, v1);
+      vload_cs(V + (size_t)(i + 2) * ldv + r, v2);
+      vload_cs(V + (size_t)(i + 3) * ldv + r, v3);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        u[e] = fma_rn(v0[e], c2s[i + 0], u[e]);
+        u[e] = fma_rn(v1[e], c2s[i + 1], u[e]);
+        u[e] = fma_rn(v2[e], c2s[i + 2], u[e]);
+        u[e] = fma_rn(v3[e], c2s[i + 3], u[e]);
+      }
+    }
+    for (; i < k; ++i) {
+      T v0[VN];
+      vload_cs(V + (size_t)i * ldv + r, v0);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) u[e] = fma_rn(v0[e], c2s[i], u[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      wv[e] = sub_rn(wv[e], u[e]);
+      ss = fma_rn(wv[e], wv[e], ss);
+    }
+    vstore(w + r, wv);
+  }
+  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads) {
+    T u = T(0);
+    for (int i = 0; i < k; ++i) u = fma_rn(__ldcs(V + (size_t)i * ldv + r), c2s[i], u);
+    const T wv = sub_rn(w[r], u);
+    w[r] = wv;
+    ss = fma_rn(wv, wv, ss);
+  }
+  const T t = block_sum(ss, red);
+  T* part = static_cast<T*>(ws.part);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  if (last_cta(ws.counter)) {
+    T s = T(0);
+    for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) {
+      const T hs = sqrt_rn(s);
+      sv.Hc(j, j + 1) = hs;
+      sv.h->h_sub = (double)hs;
+      // krylov.py:146: breakdown when h_sub <= tol * w0 (Python floats)
+      const bool brk = (double)hs <= sv.h->breakdown_tol * sv.h->w0;
+      givens_column(sv, j, sv.h->threshold, brk, m_limit);
+    }
+  }
+}
+
+// K_S: V[:, j+1] = w / h_sub (krylov.py:148; IEEE division, no reciprocal)
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_step_scale(const T* __restrict__ w, T* __restrict__ vn,
+                                                         long long n, int j, StateView<T> sv) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  const T hs = sv.Hc(j, j + 1);
+  const long long nv = n / VN;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < nv;
+       g += (long long)gridDim.x * blockDim.x) {
+    T a[VN];
+    vload(w + g * VN, a);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);
+    vstore(vn + g * VN, a);
+  }
+  for (long long r = nv * VN + blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x)
+    vn[r] = div_rn(w[r], hs);
+}
+
+// ===================================================================== start
+
+// Reset the cycle state (krylov.py:62-68, 96-100) — whole CTA.
+template <typename T>
+__device__ void init_state(const StateView<T>& sv, T gamma, double b_norm, double rtol,
+                           double btol, int extra_flags) {
+  const int m = sv.m;
+  const size_t hm = (size_t)(m + 1) * m;
+  for (size_t i = threadIdx.x; i < hm; i += blockDim.x) { sv.H[i] = T(0); sv.R[i] = T(0); }
+  for (int i = threadIdx.x; i < m + 1; i += blockDim.x) {
+    sv.g[i] = T(0); sv.c1[i] = T(0); sv.c2[i] = T(0); sv.d[i] = T(0);
+    if (i < m) { sv.cs[i] = T(0); sv.sn[i] = T(0); sv.implicit[i] = 0.0; }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sv.g[0] = gamma;
+    mpg_state_header* h = sv.h;
+    int flags = extra_flags;
+    int done = 0;
+    if (!isfinite(gamma)) { flags |= MPG_FLAG_NONFINITE_GAMMA; done = 1; }
+    if (gamma == T(0)) done = 1;                 // solvers.py:150-151
+    if (extra_flags) done = 1;
+    h->flags = flags;
+    h->steps = 0;
+    h->done = done;
+    h->breakdown = 0;
+    h->m = m;
+    h->prec = sizeof(T) == 8 ? MPG_FP64 : MPG_FP32;
+    h->gamma = (double)gamma;
+    h->b_norm = b_norm < 0 ? (double)gamma : b_norm;
+    h->threshold = rtol * h->b_norm;            // solvers.py:158
+    h->rtol = rtol;
+    h->breakdown_tol = btol;
+    h->w0 = 0.0;
+    h->h_sub = 0.0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_start(const T* __restrict__ r0, long long n,
+                                                    StateView<T> sv, double rtol,
+                                                    const double* b_norm_src, double btol,
+                                                    WsView ws) {
+  __shared__ T red[32];
+  T ss = T(0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const T v = r0[i];
+    ss = fma_rn(v, v, ss);
+  }
+  const T t = block_sum(ss, red);
+  T* part = static_cast<T*>(ws.part);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  if (last_cta(ws.counter)) {
+    T s = T(0);
+    for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
+    s = block_sum(s, red);
+    const T gamma = sqrt_rn(s);
+    // restarted cycles threshold on the outer ||b|| (solvers.py:186,198);
+    // a null source means "use gamma" (gmres_cycle with b_norm=None, r0=b)
+    const double bn = b_norm_src ? *b_norm_src : -1.0;
+    init_state(sv, gamma, bn, rtol, btol, 0);
+  }
+}
+
+// IR inner right-hand side: r32 = fp32(r64 / rho) with rho = ||r64||
+// (solvers.py:339-341), overflow check (core.py:264-271), gamma = ||r32||.
+__global__ void __launch_bounds__(kThreads) k_start_ir(const double* __restrict__ r64,
+                                                       float* __restrict__ r32, long long n,
+                                                       StateView<float> sv, double rtol,
+                                                       double btol, WsView ws) {
+  __shared__ float red[32];
+  __shared__ int ovf_s;
+  const double rho = sv.h->rnorm;
+  if (threadIdx.x == 0) ovf_s = 0;
+  __syncthreads();
+  float ss = 0.f;
+  int ovf = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double q = __ddiv_rn(r64[i], rho);
+    const float v = __double2float_rn(q);
+    ovf |= (isinf(v) && isfinite(q));
+    r32[i] = v;
+    ss = fma_rn(v, v, ss);
+  }
+  if (ovf) atomicOr(&ovf_s, 1);
+  const float t = block_sum(ss, red);
+  float* part = static_cast<float*>(ws.part);
+  if (threadIdx.x == 0) part[(size_t)blockIdx.x * 2] = t, part[(size_t)blockIdx.x * 2 + 1] = ovf_s ? 1.f : 0.f;
+  if (last_cta(ws.counter)) {
+    float s = 0.f, o = 0.f;
+    for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) {
+      s += __ldcg(part + (size_t)p * 2);
+      o += __ldcg(part + (size_t)p * 2 + 1);
+    }
+    s = block_sum(s, red);
+    o = block_sum(o, red);
+    const float gamma = sqrt_rn(s);
+    // the inner cycle's b_norm is ||r32|| itself (solvers.py:146 with b = r32)
+    init_state(sv, gamma, -1.0, rtol, btol, o > 0.f ? MPG_FLAG_OVERFLOW : 0);
+    if (threadIdx.x == 0) sv.h->rho = rho;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_start_scale(const T* __restrict__ r0, T* __restrict__ v0,
+                                                          long long n, StateView<T> sv) {
+  if (gated(sv.h)) return;
+  const T gamma = sv.g[0];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v0[i] = div_rn(r0[i], gamma);
+}
+
+// ======================================================================= lsq
+// Back-substitution R[:k,:k] d = g[:k] (krylov.py:190-202; LAPACK xTRSV 'U','N'
+// column order).  One warp.
+template <typename T>
+__global__ void k_lsq(StateView<T> sv) {
+  const int k = sv.h->steps;
+  const int lane = threadIdx.x;
+  if (k == 0 || (sv.h->flags & (MPG_FLAG_NONFINITE_OP | MPG_FLAG_NONFINITE_GAMMA | MPG_FLAG_OVERFLOW)))
+    return;
+  int bad = 0;
+  for (int i = lane; i < k; i += 32) {
+    const T r = sv.Rc(i, i);
+    bad |= (r == T(0)) || !isfinite(r);
+    sv.d[i] = sv.g[i];
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad) {
+    if (lane == 0) atomicOr(&sv.h->flags, MPG_FLAG_SINGULAR);
+    return;
+  }
+  __syncwarp();
+  for (int jj = k - 1; jj >= 0; --jj) {
+    if (lane == 0 && sv.d[jj] != T(0)) sv.d[jj] = div_rn(sv.d[jj], sv.Rc(jj, jj));
+    __syncwarp();
+    const T temp = sv.d[jj];
+    if (temp != T(0))
+      for (int i = lane; i < jj; i += 32) sv.d[i] = fma_rn(-temp, sv.Rc(jj, i), sv.d[i]);
+    __syncwarp();
+  }
+}
+
+// ================================================================== combine
+// u = V[:, :k] d (solvers.py:171) fused with the update of the iterate.
+template <typename T, typename TX, int MODE>
+__global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, long long ldv,
+                                                      long long n, StateView<T> sv, TX* x,
+                                                      const void* diag, T* u) {
+  const int k = sv.h->steps;
+  if (k == 0 || (sv.h->flags & (MPG_FLAG_NONFINITE_OP | MPG_FLAG_NONFINITE_GAMMA |
+                                 MPG_FLAG_OVERFLOW | MPG_FLAG_SINGULAR)))
+    return;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  T* ds = reinterpret_cast<T*>(smraw);
+  for (int i = threadIdx.x; i < k; i += blockDim.x) ds[i] = sv.d[i];
+  __syncthreads();
+  const double rho = sv.h->rho;
+  int bad = 0;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int i = 0; i < k; ++i) acc = fma_rn(__ldcs(V + (size_t)i * ldv + r), ds[i], acc);
+    if constexpr (MODE == CMB_STORE) {
+      u[r] = acc;
+    } else if constexpr (MODE == CMB_ADD) {
+      x[r] = add_rn(x[r], (TX)acc);
+    } else if constexpr (MODE == CMB_IR) {
+      bad |= !isfinite(acc);
+      x[r] = __dadd_rn(x[r], __dmul_rn(rho, (double)acc));
+    } else if constexpr (MODE == CMB_J1_ADD) {
+      const T y = div_rn(acc, static_cast<const T*>(diag)[r]);
+      x[r] = add_rn(x[r], (TX)y);
+    } else if constexpr (MODE == CMB_J1_IR) {
+      const T y = div_rn(acc, static_cast<const T*>(diag)[r]);
+      bad |= !isfinite(y);
+      x[r] = __dadd_rn(x[r], __dmul_rn(rho, (double)y));
+    } else if constexpr (MODE == CMB_J1_CAST) {
+      const float a32 = __double2float_rn((double)acc);
+      const float y = __fdiv_rn(a32, static_cast<const float*>(diag)[r]);
+      x[r] = __dadd_rn((double)x[r], (double)y);
+    }
+  }
+  if (bad) atomicOr(&sv.h->flags, MPG_FLAG_NONFINITE_X);
+}
+
+// ================================================================= launchers
+
+static int g_sms = 0;
+int num_sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+static unsigned grid_stream(long long n, int per_sm = 8) {
+  long long g = (n + kThreads - 1) / kThreads;
+  const long long cap = (long long)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+template <typename T>
+cudaError_t launch_dot1_w(const T* w, long long n, const T* V, long long ldv, int k,
+                          StateView<T> sv, WsView ws, cudaStream_t st) {
+  long long G = (n + 2047) / 2048;
+  const long long cap = (long long)num_sms() * 4;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_dot1_w<T><<<(unsigned)G, kThreads, 0, st>>>(w, n, V, ldv, k, sv, ws);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* w,
+                              StateView<T> sv, WsView ws, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_update_dot<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  const size_t sz = sizeof(T);
+  const size_t budget = 200 * 1024;
+  const size_t tail = 16 * 8 + (size_t)(2 * k + 8 + 32) * sz + 64;
+  // tile rows: grow while a stage stays <= 48 KB; shrink while 2 stages do not fit
+  int TB = 256;
+  while (TB < 2048 && (size_t)(k + 1) * (TB * 2) * sz <= 48 * 1024) TB *= 2;
+  while (TB > 32 && 2 * (size_t)(k + 1) * TB * sz + tail > budget) TB /= 2;
+  if (2 * (size_t)(k + 1) * TB * sz + tail > budget) return cudaErrorInvalidConfiguration;
+  const size_t stage = (size_t)(k + 1) * TB * sz;
+  int S = (int)std::min<size_t>(4, (budget - tail) / stage);
+  if (S < 2) S = 2;
+  const size_t smem = (size_t)S * stage + tail;
+  int occ = (int)((228 * 1024) / (smem + 1024));
+  if (occ < 1) occ = 1;
+  if (occ > 4) occ = 4;
+  long long tiles = (n + TB - 1) / TB;
+  long long G = (long long)num_sms() * occ;
+  if (tiles < G) G = tiles;
+  if (G > kMaxParts) G = kMaxParts;
+  if (G < 1) G = 1;
+  count_launch();
+  k_update_dot<T><<<(unsigned)G, kUdThreads, smem, st>>>(V, ldv, n, k, w, sv, ws, TB, S);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_update_norm(const T* V, long long ldv, long long n, int j, T* w,
+                               StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_update_norm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (kMaxM + 8) * (int)sizeof(T));
+  });
+  constexpr int VN = Vec<T>::n;
+  long long G = (n + (long long)kThreads * VN - 1) / ((long long)kThreads * VN);
+  const long long cap = (long long)num_sms() * 6;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_update_norm<T><<<(unsigned)G, kThreads, (size_t)(j + 9) * sizeof(T), st>>>(V, ldv, n, j, w, sv, ws,
+                                                                                 m_limit);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_step_scale(const T* w, T* vnext, long long n, int j, StateView<T> sv,
+                              cudaStream_t st) {
+  count_launch();
+  k_step_scale<T><<<grid_stream((n + Vec<T>::n - 1) / Vec<T>::n), kThreads, 0, st>>>(w, vnext, n, j, sv);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_start(const T* r0, long long n, StateView<T> sv, double rtol,
+                         const double* b_norm_src, double btol, WsView ws, cudaStream_t st) {
+  count_launch();
+  k_start<T><<<grid_stream(n, 4), kThreads, 0, st>>>(r0, n, sv, rtol, b_norm_src, btol, ws);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_start_ir(const double* r64, float* r32, long long n, StateView<float> sv,
+                            double rtol, double btol, WsView ws, cudaStream_t st) {
+  count_launch();
+  k_start_ir<<<grid_stream(n, 4), kThreads, 0, st>>>(r64, r32, n, sv, rtol, btol, ws);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_start_scale(const T* r0, T* v0, long long n, StateView<T> sv, cudaStream_t st) {
+  count_launch();
+  k_start_scale<T><<<grid_stream(n), kThreads, 0, st>>>(r0, v0, n, sv);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_lsq(StateView<T> sv, cudaStream_t st) {
+  count_launch();
+  k_lsq<T><<<1, 32, 0, st>>>(sv);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> sv, int mode,
+                           void* x, const void* diag, T* u, cudaStream_t st) {
+  const unsigned G = grid_stream(n);
+  const size_t smem = (size_t)(sv.m + 1) * sizeof(T);
+  count_launch();
+  switch (mode) {
+    case CMB_STORE:
+      k_combine<T, T, CMB_STORE><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (T*)x, diag, u);
+      break;
+    case CMB_ADD:
+      k_combine<T, T, CMB_ADD><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (T*)x, diag, u);
+      break;
+    case CMB_J1_ADD:
+      k_combine<T, T, CMB_J1_ADD><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (T*)x, diag, u);
+      break;
+    case CMB_IR:
+      if constexpr (sizeof(T) == 4)
+        k_combine<T, double, CMB_IR><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (double*)x, diag, u);
+      else
+        return cudaErrorInvalidValue;
+      break;
+    case CMB_J1_IR:
+      if constexpr (sizeof(T) == 4)
+        k_combine<T, double, CMB_J1_IR><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (double*)x, diag, u);
+      else
+        return cudaErrorInvalidValue;
+      break;
+    case CMB_J1_CAST:
+      if constexpr (sizeof(T) == 8)
+        k_combine<T, double, CMB_J1_CAST><<<G, kThreads, smem, st>>>(V, ldv, n, sv, (double*)x, diag, u);
+      else
+        return cudaErrorInvalidValue;
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+#define INST(T)                                                                                  \
+  template cudaError_t launch_dot1_w<T>(const T*, long long, const T*, long long, int,          \
+                                        StateView<T>, WsView, cudaStream_t);                   \
+  template cudaError_t launch_update_dot<T>(const T*, long long, long long, int, T*,            \
+                                            StateView<T>, WsView, cudaStream_t);               \
+  template cudaError_t launch_update_norm<T>(const T*, long long, long long, int, T*,           \
+                                             StateView<T>, WsView, int, cudaStream_t);         \
+  template cudaError_t launch_step_scale<T>(const T*, T*, long long, int, StateView<T>,         \
+                                            cudaStream_t);                                     \
+  template cudaError_t launch_start<T>(const T*, long long, StateView<T>, double, const double*, \
+                                       double, WsView, cudaStream_t);                          \
+  template cudaError_t launch_start_scale<T>(const T*, T*, long long, StateView<T>,             \
+                                             cudaStream_t);                                    \
+  template cudaError_t launch_lsq<T>(StateView<T>, cudaStream_t);                               \
+  template cudaError_t launch_combine<T>(const T*, long long, long long, StateView<T>, int,     \
+                                         void*, const void*, T*, cudaStream_t);
+INST(float)
+INST(double)
+#undef INST
+
+}  // namespace mpg

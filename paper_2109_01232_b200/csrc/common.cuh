@@ -1,0 +1,232 @@
+// Shared device helpers for the B200 mixed-precision GMRES kernels (sm_100a).
+//
+// Conventions
+//  * T is float (fp32 working precision) or double (fp64).
+//  * Every vector the library owns is padded to `ld` elements (a multiple of
+//    64), so 16-byte vector loads and TMA bulk copies never run past an
+//    allocation.  CSR arrays are 16-byte aligned with >= 16 bytes of
+//    readable padding (the Python layer guarantees both).
+//  * Reductions are deterministic: per-CTA partials in a fixed order, then a
+//    fixed-order grid finalisation by the last CTA to arrive (no float
+//    atomics), so repeated runs are bitwise identical.
+//  * Parity-critical arithmetic (SpMV products/sums, Givens scalars, the IR
+//    correction, preconditioner epilogues) uses explicit _rn intrinsics so
+//    nvcc never contracts a multiply and an add into an FMA.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mpgmres_b200.h"
+
+namespace mpg {
+
+constexpr int kThreads = 256;           // threads per CTA for streaming kernels
+constexpr int kWarps = kThreads / 32;
+constexpr int kRowAlign = 32;           // CTA row ranges start on 32-row boundaries
+
+// ---------------------------------------------------------------------------
+// exact-rounding scalar ops (no FMA contraction)
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float sqrt_rn(float a) { return __fsqrt_rn(a); }
+__device__ __forceinline__ double sqrt_rn(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <typename T> struct Vec;           // 16-byte vector of T
+template <> struct Vec<float> { using type = float4; static constexpr int n = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int n = 2; };
+
+template <typename T>
+__device__ __forceinline__ void vload(const T* p, T (&v)[Vec<T>::n]) {
+  auto q = __ldg(reinterpret_cast<const typename Vec<T>::type*>(p));
+  if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
+  else { v[0] = q.x; v[1] = q.y; }
+}
+// streaming (evict-first) load: for data read exactly once per kernel
+template <typename T>
+__device__ __forceinline__ void vload_cs(const T* p, T (&v)[Vec<T>::n]) {
+  auto q = __ldcs(reinterpret_cast<const typename Vec<T>::type*>(p));
+  if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
+  else { v[0] = q.x; v[1] = q.y; }
+}
+template <typename T>
+__device__ __forceinline__ void vload_smem(const T* p, T (&v)[Vec<T>::n]) {
+  auto q = *reinterpret_cast<const typename Vec<T>::type*>(p);
+  if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
+  else { v[0] = q.x; v[1] = q.y; }
+}
+template <typename T>
+__device__ __forceinline__ void vstore(T* p, const T (&v)[Vec<T>::n]) {
+  typename Vec<T>::type q;
+  if constexpr (Vec<T>::n == 4) { q.x = v[0]; q.y = v[1]; q.z = v[2]; q.w = v[3]; }
+  else { q.x = v[0]; q.y = v[1]; }
+  *reinterpret_cast<typename Vec<T>::type*>(p) = q;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic reductions
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed-tree block sum; result valid in every thread.  `red` needs kWarps slots.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  T t = (l < (int)(blockDim.x >> 5)) ? red[l] : T(0);
+  t = warp_sum(t);
+  return t;
+}
+
+// Last-CTA election after each CTA has published its partials.
+// Returns true in every thread of the last CTA to arrive.  The counter is
+// reset by the elected CTA so the slot can be reused by the next kernel on
+// the same stream.
+__device__ __forceinline__ bool last_cta(unsigned int* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    is_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+  return is_last;
+}
+
+// Sum `ncols` columns of a [nparts][stride] partial array in a fixed order.
+// Executed by one whole CTA; column c's total lands in out[c] (any writer).
+// Warp w handles columns c = w, w + kWarps, ...; lanes stride over parts.
+template <typename T, typename OutF>
+__device__ __forceinline__ void finalize_columns(const T* part, int nparts, int stride,
+                                                 int ncols, OutF out) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int c = w; c < ncols; c += (int)(blockDim.x >> 5)) {
+    T s = T(0);
+    for (int p = l; p < nparts; p += 32) s += __ldcg(part + (size_t)p * stride + c);
+    s = warp_sum(s);
+    if (l == 0) out(c, s);
+  }
+}
+
+// Contiguous, 32-row aligned partition of [0, n) over gridDim.x CTAs.
+__device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& r1) {
+  const long long G = gridDim.x, c = blockIdx.x;
+  r0 = (c * n / G) & ~(long long)(kRowAlign - 1);
+  r1 = (c + 1 == G) ? n : (((c + 1) * n / G) & ~(long long)(kRowAlign - 1));
+  if (r1 < r0) r1 = r0;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk global->shared copy; dst/src 16-byte aligned, bytes % 16 == 0.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// numpy add.reduceat row order (spmv.py:63-70): y = p0 + pairwise(p1..p_{L-1})
+// where pairwise is numpy's pairwise_sum: sequential from -0.0 below 8 terms,
+// 8 interleaved accumulators up to 128, recursive halving above.
+
+template <typename T, typename Get>
+__device__ __noinline__ T pairwise_long(const Get& get, int i0, int n);
+
+template <typename T, typename Get>
+__device__ __forceinline__ T pairwise(const Get& get, int i0, int n) {
+  if (n < 8) {
+    T r = T(-0.0);
+    for (int i = 0; i < n; ++i) r = add_rn(r, get(i0 + i));
+    return r;
+  }
+  return pairwise_long<T>(get, i0, n);
+}
+
+template <typename T, typename Get>
+__device__ __noinline__ T pairwise_long(const Get& get, int i0, int n) {
+  if (n <= 128) {
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = get(i0 + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], get(i0 + i + j));
+    }
+    T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])),
+                   add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
+    for (; i < n; ++i) res = add_rn(res, get(i0 + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  T a = pairwise_long<T>(get, i0, n2);
+  T b = (n - n2 < 8) ? pairwise<T>(get, i0 + n2, n - n2) : pairwise_long<T>(get, i0 + n2, n - n2);
+  return add_rn(a, b);
+}
+
+template <typename T, typename Get>
+__device__ __forceinline__ T row_reduce(const Get& get, int len) {
+  if (len <= 0) return T(0);
+  T p0 = get(0);
+  if (len == 1) return p0;
+  return add_rn(p0, pairwise<T>(get, 1, len - 1));
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers (host)
+int num_sms();
+int grid_for(long long rows, int rows_per_tile, int ctas_per_sm);
+
+}  // namespace mpg

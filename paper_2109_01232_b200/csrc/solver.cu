@@ -1,0 +1,334 @@
+// Native solver driver: enqueues whole restart cycles (solvers.py:122-227,
+// 297-384) on the device and replays them as CUDA graphs.  The host reads
+// the cycle's scalar record (state header + implicit residuals) once per
+// cycle; nothing inside a cycle synchronises with the host — the reference's
+// per-step Python `break` (solvers.py:164-168) is a device-side done flag.
+#include <map>
+#include <vector>
+
+#include "spmv.cuh"
+#include "state.cuh"
+
+struct mpg_solver {
+  mpg_solver_desc d;
+  std::vector<mpg_poly_op> ops;
+  std::map<int, cudaGraphExec_t> graphs;  // per m_limit
+  std::map<int, int> graph_launches;      // kernels per graph (for the launch counter)
+  cudaStream_t cap = nullptr;
+};
+
+namespace mpg {
+
+// Optional per-kernel-class CUDA-event profiling of an eager cycle.
+struct Prof {
+  cudaStream_t st;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+};
+static thread_local Prof* t_prof = nullptr;
+struct ProfScope {
+  int k;
+  cudaEvent_t a = nullptr;
+  explicit ProfScope(int kind) : k(kind) {
+    if (t_prof) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, t_prof->st);
+    }
+  }
+  ~ProfScope() {
+    if (t_prof) {
+      cudaEvent_t b;
+      cudaEventCreate(&b);
+      cudaEventRecord(b, t_prof->st);
+      t_prof->ev.push_back({k, {a, b}});
+    }
+  }
+};
+enum { PK_START = 0, PK_PRECOND, PK_SPMV_DOT, PK_UPDATE_DOT, PK_UPDATE_NORM, PK_SCALE, PK_FINISH,
+       PK_RESIDUAL, PK_COUNT };
+
+#define TRY(...)                       \
+  do {                                   \
+    cudaError_t e_ = (__VA_ARGS__);      \
+    if (e_ != cudaSuccess) return e_;    \
+  } while (0)
+
+static mpg_state_header* hdr_of(const mpg_solver_desc& d) {
+  return static_cast<mpg_state_header*>(d.state);
+}
+
+// Run a lowered polynomial program on x -> y with scratch t0..t2, in TP.
+template <typename TP>
+static cudaError_t run_poly(const mpg_solver_desc& d, const std::vector<mpg_poly_op>& ops,
+                            const TP* vals, const TP* x, TP* y, TP* t0, TP* t1, TP* t2,
+                            const mpg_state_header* gate, WsView ws, cudaStream_t st) {
+  CsrView<TP> A{d.row_ptr, d.col_idx, vals, d.n};
+  TP* bufs[5] = {const_cast<TP*>(x), y, t0, t1, t2};
+  for (const mpg_poly_op& op : ops) {
+    switch (op.op) {
+      case MPG_POLY_SCALE:
+      case MPG_POLY_ACC:
+      case MPG_POLY_ZERO:
+        TRY(launch_poly_elem<TP>(op.op, (TP)op.a, bufs[op.src], bufs[op.dst], y, d.n, gate, st));
+        break;
+      default:
+        TRY(launch_poly_op<TP>(A, op, x, y, t0, t1, t2, gate, d.n, ws, st));
+    }
+  }
+  return cudaSuccess;
+}
+
+// z = M^{-1} v for the Arnoldi operator (solvers.py:159: op = A(M^{-1} v)).
+// Returns the buffer holding z (v itself when there is no preconditioner).
+template <typename T>
+static cudaError_t precond_apply(const mpg_solver& s, const T* v, const T** z, WsView ws,
+                                 const mpg_state_header* gate, cudaStream_t st) {
+  const mpg_solver_desc& d = s.d;
+  *z = v;
+  if (d.pc_kind == MPG_PC_NONE) return cudaSuccess;
+  const bool cast = d.pc_prec != d.prec;  // fp32 preconditioner in an fp64 solve
+  if (!cast) {
+    T* out = static_cast<T*>(d.pc_t0);
+    if (d.pc_kind == MPG_PC_JACOBI) {
+      TRY(launch_jacobi<T>(d.n, d.pc_block, static_cast<const T*>(d.pc_lu), d.pc_piv, v, out, gate, st));
+    } else {
+      TRY(run_poly<T>(d, s.ops, static_cast<const T*>(d.pc_values), v, out,
+                      static_cast<T*>(d.pc_t1), static_cast<T*>(d.pc_t2), static_cast<T*>(d.pc_t3),
+                      gate, ws, st));
+    }
+    *z = out;
+    return cudaSuccess;
+  }
+  if constexpr (sizeof(T) == 8) {
+    // cast_apply (precond.py:393-414): narrow, apply in fp32, widen
+    float* v32 = static_cast<float*>(d.pc_t0);
+    float* y32 = static_cast<float*>(d.pc_t1);
+    TRY(launch_cast_gated<double, float>(v, v32, d.n, gate, ws.scratch_i64, st));
+    if (d.pc_kind == MPG_PC_JACOBI) {
+      TRY(launch_jacobi<float>(d.n, d.pc_block, static_cast<const float*>(d.pc_lu), d.pc_piv, v32, y32, gate, st));
+    } else {
+      TRY(run_poly<float>(d, s.ops, static_cast<const float*>(d.pc_values), v32, y32,
+                          static_cast<float*>(d.pc_t2), static_cast<float*>(d.pc_t3),
+                          static_cast<float*>(d.pc_t4), gate, ws, st));
+    }
+    T* out = static_cast<T*>(d.u);
+    TRY(launch_cast_gated<float, double>(y32, out, d.n, gate, nullptr, st));
+    *z = out;
+    return cudaSuccess;
+  }
+  return cudaErrorInvalidValue;
+}
+
+// End of cycle: d = R^{-1} g ; x <- x + M^{-1}(V d)   (solvers.py:169-174, 357)
+template <typename T>
+static cudaError_t finish_cycle(const mpg_solver& s, StateView<T> sv, WsView ws, cudaStream_t st) {
+  const mpg_solver_desc& d = s.d;
+  const T* V = static_cast<const T*>(d.V);
+  TRY(launch_lsq<T>(sv, st));
+  const bool ir = d.mode == MPG_MODE_IR;
+  const bool cast = d.pc_kind != MPG_PC_NONE && d.pc_prec != d.prec;
+  if (d.pc_kind == MPG_PC_NONE)
+    return launch_combine<T>(V, d.ldv, d.n, sv, ir ? CMB_IR : CMB_ADD, d.x, nullptr, nullptr, st);
+  if (d.pc_kind == MPG_PC_JACOBI && d.pc_block == 1) {
+    const int mode = cast ? CMB_J1_CAST : (ir ? CMB_J1_IR : CMB_J1_ADD);
+    return launch_combine<T>(V, d.ldv, d.n, sv, mode, d.x, d.pc_lu, nullptr, st);
+  }
+  // general: u = V d, z = M^{-1} u (ungated), x += z
+  T* u = static_cast<T*>(d.u);
+  TRY(launch_combine<T>(V, d.ldv, d.n, sv, CMB_STORE, nullptr, nullptr, u, st));
+  if (!cast) {
+    T* z = static_cast<T*>(d.pc_t0);
+    if (d.pc_kind == MPG_PC_JACOBI)
+      TRY(launch_jacobi<T>(d.n, d.pc_block, static_cast<const T*>(d.pc_lu), d.pc_piv, u, z, nullptr, st));
+    else
+      TRY(run_poly<T>(d, s.ops, static_cast<const T*>(d.pc_values), u, z, static_cast<T*>(d.pc_t1),
+                      static_cast<T*>(d.pc_t2), static_cast<T*>(d.pc_t3), nullptr, ws, st));
+    if (ir) {
+      if constexpr (sizeof(T) == 4)
+        return launch_finish_add<float, double>(static_cast<double*>(d.x), z, d.n, sv.h, 1, st);
+      return cudaErrorInvalidValue;
+    }
+    return launch_finish_add<T, T>(static_cast<T*>(d.x), z, d.n, sv.h, 0, st);
+  }
+  if constexpr (sizeof(T) == 8) {
+    float* u32 = static_cast<float*>(d.pc_t0);
+    float* y32 = static_cast<float*>(d.pc_t1);
+    TRY(launch_cast_gated<double, float>(u, u32, d.n, nullptr, ws.scratch_i64, st));
+    if (d.pc_kind == MPG_PC_JACOBI)
+      TRY(launch_jacobi<float>(d.n, d.pc_block, static_cast<const float*>(d.pc_lu), d.pc_piv, u32, y32, nullptr, st));
+    else
+      TRY(run_poly<float>(d, s.ops, static_cast<const float*>(d.pc_values), u32, y32,
+                          static_cast<float*>(d.pc_t2), static_cast<float*>(d.pc_t3),
+                          static_cast<float*>(d.pc_t4), nullptr, ws, st));
+    return launch_finish_add<float, double>(static_cast<double*>(d.x), y32, d.n, sv.h, 2, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t st) {
+  const mpg_solver_desc& d = s.d;
+  StateView<T> sv = make_state<T>(d.state, d.m);
+  WsView ws = make_ws(d.ws);
+  T* V = static_cast<T*>(d.V);
+  T* w = static_cast<T*>(d.w);
+  CsrView<T> A{d.row_ptr, d.col_idx, static_cast<const T*>(d.values), d.n};
+  mpg_state_header* h = hdr_of(d);
+  // cycle start: gamma, V[:,0] = r0 / gamma
+  {
+  ProfScope ps(PK_START);
+  if (d.mode == MPG_MODE_IR) {
+    if constexpr (sizeof(T) == 4) {
+      TRY(launch_start_ir(static_cast<const double*>(d.r), static_cast<float*>(d.r_in), d.n, sv,
+                          d.rtol, d.breakdown_tol, ws, st));
+      TRY(launch_start_scale<T>(static_cast<const T*>(d.r_in), V, d.n, sv, st));
+    } else {
+      return cudaErrorInvalidValue;
+    }
+  } else {
+    TRY(launch_start<T>(static_cast<const T*>(d.r), d.n, sv, d.rtol, &h->outer_b_norm,
+                        d.breakdown_tol, ws, st));
+    TRY(launch_start_scale<T>(static_cast<const T*>(d.r), V, d.n, sv, st));
+  }
+  }
+  for (int j = 0; j < m_limit; ++j) {
+    const T* vj = V + (size_t)j * d.ldv;
+    const T* z = nullptr;
+    { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
+    { ProfScope ps(PK_SPMV_DOT); TRY(launch_spmv_dot1<T>(A, z, w, V, d.ldv, j + 1, sv, ws, st)); }
+    { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, w, sv, ws, st)); }
+    { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, w, sv, ws, m_limit, st)); }
+    { ProfScope ps(PK_SCALE); TRY(launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st)); }
+  }
+  { ProfScope ps(PK_FINISH); TRY(finish_cycle<T>(s, sv, ws, st)); }
+  ProfScope ps(PK_RESIDUAL);
+  // explicit residual in the outer precision (solvers.py:205 / :358)
+  if (d.mode == MPG_MODE_IR) {
+    CsrView<double> A64{d.row_ptr, d.col_idx, d.values64, d.n};
+    return launch_residual<double>(A64, static_cast<const double*>(d.b), static_cast<const double*>(d.x),
+                                   static_cast<double*>(d.r), nullptr, h, ws, st);
+  }
+  return launch_residual<T>(A, static_cast<const T*>(d.b), static_cast<const T*>(d.x),
+                            static_cast<T*>(d.r), nullptr, h, ws, st);
+}
+
+static cudaError_t enqueue_any(const mpg_solver& s, int m_limit, cudaStream_t st) {
+  return s.d.prec == MPG_FP64 ? enqueue_cycle<double>(s, m_limit, st)
+                              : enqueue_cycle<float>(s, m_limit, st);
+}
+
+}  // namespace mpg
+
+using namespace mpg;
+
+extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) {
+  if (!desc || !out) return MPG_EARG;
+  const mpg_solver_desc& d = *desc;
+  if (d.m < 1 || d.m > kMaxM || d.n < 1 || d.ldv < d.n || d.ldv % 64) return MPG_EARG;
+  if (d.prec != MPG_FP32 && d.prec != MPG_FP64) return MPG_EARG;
+  if (d.mode == MPG_MODE_IR && (d.prec != MPG_FP32 || !d.values64 || !d.r_in)) return MPG_EARG;
+  if (!d.row_ptr || !d.col_idx || !d.values || !d.x || !d.b || !d.r || !d.V || !d.w || !d.state || !d.ws)
+    return MPG_EARG;
+  if (d.pc_kind != MPG_PC_NONE) {
+    if (d.pc_prec != d.prec && !(d.pc_prec == MPG_FP32 && d.prec == MPG_FP64)) return MPG_EUNSUPPORTED;
+    if (d.pc_kind == MPG_PC_JACOBI && (!d.pc_lu || d.pc_block < 1 || d.pc_block > 32)) return MPG_EARG;
+    if (d.pc_kind == MPG_PC_JACOBI && d.pc_block > 1 && !d.pc_piv) return MPG_EARG;
+    if (d.pc_kind == MPG_PC_POLY && (!d.pc_ops || d.pc_nops < 1 || !d.pc_values)) return MPG_EARG;
+    if (!d.pc_t0 || !d.pc_t1) return MPG_EARG;
+  }
+  mpg_solver* s = new mpg_solver();
+  s->d = d;
+  if (d.pc_kind == MPG_PC_POLY) s->ops.assign(d.pc_ops, d.pc_ops + d.pc_nops);
+  s->d.pc_ops = nullptr;
+  if (cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking) != cudaSuccess) {
+    delete s;
+    return (int)cudaGetLastError();
+  }
+  *out = s;
+  return MPG_OK;
+}
+
+extern "C" int mpg_solver_destroy(mpg_solver* s) {
+  if (!s) return MPG_OK;
+  for (auto& kv : s->graphs) cudaGraphExecDestroy(kv.second);
+  if (s->cap) cudaStreamDestroy(s->cap);
+  delete s;
+  return MPG_OK;
+}
+
+extern "C" int mpg_solver_begin(mpg_solver* s, void* stream) {
+  if (!s) return MPG_ESTATE;
+  const mpg_solver_desc& d = s->d;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  WsView ws = make_ws(d.ws);
+  mpg_state_header* h = hdr_of(d);
+  const bool outer64 = d.mode == MPG_MODE_IR || d.prec == MPG_FP64;
+  cudaError_t e;
+  if (outer64) {
+    e = launch_norm2<double>(static_cast<const double*>(d.b), d.n, &h->outer_b_norm, ws, st);
+    if (e) return e;
+    const double* vals = d.mode == MPG_MODE_IR ? d.values64 : static_cast<const double*>(d.values);
+    CsrView<double> A{d.row_ptr, d.col_idx, vals, d.n};
+    e = launch_residual<double>(A, static_cast<const double*>(d.b), static_cast<const double*>(d.x),
+                                static_cast<double*>(d.r), nullptr, h, ws, st);
+  } else {
+    e = launch_norm2<float>(static_cast<const float*>(d.b), d.n, &h->outer_b_norm, ws, st);
+    if (e) return e;
+    CsrView<float> A{d.row_ptr, d.col_idx, static_cast<const float*>(d.values), d.n};
+    e = launch_residual<float>(A, static_cast<const float*>(d.b), static_cast<const float*>(d.x),
+                               static_cast<float*>(d.r), nullptr, h, ws, st);
+  }
+  return (int)e;
+}
+
+extern "C" int mpg_solver_cycle(mpg_solver* s, int32_t m_limit, void* stream) {
+  if (!s) return MPG_ESTATE;
+  if (m_limit < 1 || m_limit > s->d.m) return MPG_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!s->d.use_graph) return (int)enqueue_any(*s, m_limit, st);
+  auto it = s->graphs.find(m_limit);
+  if (it == s->graphs.end()) {
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeRelaxed);
+    if (e) return e;
+    const int64_t before = mpg_launch_count();
+    e = enqueue_any(*s, m_limit, s->cap);
+    cudaError_t e2 = cudaStreamEndCapture(s->cap, &g);
+    if (e) { if (g) cudaGraphDestroy(g); return e; }
+    if (e2) return e2;
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e) return e;
+    it = s->graphs.emplace(m_limit, ex).first;
+    s->graph_launches[m_limit] = (int)(mpg_launch_count() - before);
+    count_launch(-(int)(mpg_launch_count() - before));  // capture is not execution
+  }
+  cudaError_t e = cudaGraphLaunch(it->second, st);
+  if (e == cudaSuccess) count_launch(s->graph_launches[m_limit]);
+  return (int)e;
+}
+
+extern "C" int mpg_solver_profile_cycle(mpg_solver* s, int32_t m_limit, void* stream,
+                                        double* ms_out, int32_t* launches_out) {
+  if (!s || !ms_out) return MPG_EARG;
+  if (m_limit < 1 || m_limit > s->d.m) return MPG_EARG;
+  Prof p;
+  p.st = static_cast<cudaStream_t>(stream);
+  t_prof = &p;
+  cudaError_t e = enqueue_any(*s, m_limit, p.st);
+  t_prof = nullptr;
+  cudaError_t e2 = cudaStreamSynchronize(p.st);
+  for (int k = 0; k < PK_COUNT; ++k) {
+    ms_out[k] = 0.0;
+    if (launches_out) launches_out[k] = 0;
+  }
+  for (auto& r : p.ev) {
+    float ms = 0.f;
+    if (!e && !e2) cudaEventElapsedTime(&ms, r.second.first, r.second.second);
+    ms_out[r.first] += ms;
+    if (launches_out) launches_out[r.first] += 1;
+    cudaEventDestroy(r.second.first);
+    cudaEventDestroy(r.second.second);
+  }
+  return (int)(e ? e : e2);
+}

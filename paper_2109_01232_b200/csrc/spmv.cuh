@@ -1,0 +1,223 @@
+// CSR SpMV tile pipeline for sm_100a.
+//
+// Each persistent CTA owns a contiguous, 32-row-aligned slice of rows and
+// walks it in tiles of kSpTile rows.  One producer warp streams each tile's
+// row_ptr slice, col_idx range and values range into shared memory with 1-D
+// TMA bulk copies (cp.async.bulk -> UBLKCP) into a 2-stage ring guarded by
+// full/empty mbarriers; eight consumer warps compute one row per thread with
+// the reference's exact summation order (common.cuh: row_reduce), gathering
+// x through the read-only path.  A tile whose nnz range does not fit the
+// stage falls back to direct global loads (long-row matrices).
+//
+// Epilogue policy (template parameter E):
+//   T   on_row(long long r, T y)              per row, by the computing thread
+//   void on_tile(long long a, int nrows, const T* ys)   all consumers, after a
+//                                              consumer barrier (ys complete)
+//   void on_end()                              all consumers, after the last tile
+//
+// Reference: spmv.py:48-72 (products rounded, rows reduced by add.reduceat).
+#pragma once
+
+#include "common.cuh"
+
+namespace mpg {
+
+constexpr int kSpTile = 512;                   // rows per tile
+constexpr int kSpCap = 8 * kSpTile + 32;       // staged entries per stage
+constexpr int kSpStages = 2;
+constexpr int kSpConsumers = 256;
+constexpr int kSpConsumerWarps = kSpConsumers / 32;
+constexpr int kSpThreads = kSpConsumers + 32;  // + 1 producer warp
+
+template <typename T>
+struct CsrView {
+  const int32_t* rp;
+  const int32_t* ci;
+  const T* v;
+  long long n;
+};
+
+template <typename T>
+struct alignas(128) SpSmem {
+  alignas(16) int32_t rp[kSpStages][kSpTile + 8];
+  alignas(16) int32_t ci[kSpStages][kSpCap];
+  alignas(16) T v[kSpStages][kSpCap];
+  alignas(16) T ys[2][kSpTile];
+  uint64_t full[kSpStages];
+  uint64_t empty[kSpStages];
+  int32_t meta[kSpStages][4];  // base, off_ci, off_v, staged
+  T red[32];
+  T acc[8];
+};
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kSpConsumers) : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T consumer_block_sum(T v, T* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  consumer_sync();
+  if (l == 0) red[w] = v;
+  consumer_sync();
+  T t = (l < kSpConsumerWarps) ? red[l] : T(0);
+  return warp_sum(t);
+}
+
+__device__ __forceinline__ long long round16(long long b) { return (b + 15) & ~15LL; }
+
+// Accumulate acc[i] += sum_r V_i[r] * y[r] over one tile for i < k, with a
+// deterministic (tile-independent) combination order.  V_i(i) returns the
+// tile start of basis vector i; y is the tile in shared memory.
+enum { kLoadLdg = 0, kLoadStream = 1, kLoadShared = 2 };
+
+template <typename T, int kLoad, typename VRow>
+__device__ __forceinline__ void tile_dots(int k, int nr, const VRow& vrow, const T* y, T* acc,
+                                          T* pw) {
+  constexpr int VN = Vec<T>::n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ng = nr / VN;
+  auto range_dot = [&](const T* v, int g0, int g1, bool tail) -> T {
+    T p = T(0);
+#pragma unroll 4
+    for (int g = g0 + lane; g < g1; g += 32) {
+      T a[VN], b[VN];
+      if (kLoad == kLoadStream) vload_cs(v + (size_t)g * VN, a);
+      else if (kLoad == kLoadLdg) vload(v + (size_t)g * VN, a);
+      else vload_smem(v + (size_t)g * VN, a);
+      const T* yy = y + g * VN;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) b[e] = yy[e];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) p = fma_rn(a[e], b[e], p);
+    }
+    if (tail) {
+      const int r = ng * VN + lane;
+      if (r < nr) p = fma_rn(kLoad == kLoadStream ? __ldcs(v + r) : (kLoad == kLoadLdg ? __ldg(v + r) : v[r]), y[r], p);
+    }
+    return warp_sum(p);
+  };
+  if (k >= kSpConsumerWarps) {
+    for (int i = warp; i < k; i += kSpConsumerWarps) {
+      T p = range_dot(vrow(i), 0, ng, true);
+      if (lane == 0) acc[i] += p;
+    }
+  } else {
+    const int nc = kSpConsumerWarps / k;
+    T p = T(0);
+    if (warp < k * nc) {
+      const int i = warp / nc, c = warp % nc;
+      const int g0 = (int)((long long)ng * c / nc), g1 = (int)((long long)ng * (c + 1) / nc);
+      p = range_dot(vrow(i), g0, g1, c == nc - 1);
+    }
+    if (lane == 0) pw[warp] = p;
+    consumer_sync();
+    if ((int)threadIdx.x < k) {
+      T s = T(0);
+      for (int c = 0; c < nc; ++c) s += pw[threadIdx.x * nc + c];
+      acc[threadIdx.x] += s;
+    }
+  }
+}
+
+template <typename T, typename E>
+__device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __restrict__ x,
+                                              E& epi, SpSmem<T>& sm) {
+  long long R0, R1;
+  cta_rows(A.n, R0, R1);
+  const int nt = (int)((R1 - R0 + kSpTile - 1) / kSpTile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSpStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kSpConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kSpConsumerWarps) {
+    // ------------------------------ producer warp ------------------------------
+    if (lane == 0) {
+      long long nb_a = R0, nb_b = (nt > 0) ? min(R0 + kSpTile, R1) : R0;
+      int next_base = (nt > 0) ? __ldg(A.rp + nb_a) : 0;
+      int next_end = (nt > 0) ? __ldg(A.rp + nb_b) : 0;
+      for (int t = 0; t < nt; ++t) {
+        const int s = t % kSpStages;
+        const long long a = nb_a, b = nb_b;
+        const int base = next_base, end = next_end;
+        // prefetch the bounds of the following tile while this one streams in
+        if (t + 1 < nt) {
+          nb_a = a + kSpTile;
+          nb_b = min(nb_a + kSpTile, R1);
+          next_base = end;
+          next_end = __ldg(A.rp + nb_b);
+        }
+        if (t >= kSpStages) mbar_wait(&sm.empty[s], ((t / kSpStages) - 1) & 1);
+        const long long ci_lo = ((long long)base * 4) & ~15LL;
+        const long long ci_hi = round16((long long)end * 4);
+        const long long v_lo = ((long long)base * (long long)sizeof(T)) & ~15LL;
+        const long long v_hi = round16((long long)end * (long long)sizeof(T));
+        const bool staged = (ci_hi - ci_lo) <= (long long)kSpCap * 4 &&
+                            (v_hi - v_lo) <= (long long)kSpCap * (long long)sizeof(T);
+        sm.meta[s][0] = base;
+        sm.meta[s][1] = base - (int)(ci_lo / 4);
+        sm.meta[s][2] = base - (int)(v_lo / (long long)sizeof(T));
+        sm.meta[s][3] = staged ? 1 : 0;
+        const uint32_t rp_bytes = (uint32_t)round16((b - a + 1) * 4);
+        uint32_t total = rp_bytes;
+        if (staged) total += (uint32_t)(ci_hi - ci_lo) + (uint32_t)(v_hi - v_lo);
+        fence_proxy_async();
+        mbar_expect_tx(&sm.full[s], total);
+        bulk_g2s(sm.rp[s], A.rp + a, rp_bytes, &sm.full[s]);
+        if (staged) {
+          if (ci_hi > ci_lo)
+            bulk_g2s(sm.ci[s], reinterpret_cast<const char*>(A.ci) + ci_lo,
+                     (uint32_t)(ci_hi - ci_lo), &sm.full[s]);
+          if (v_hi > v_lo)
+            bulk_g2s(sm.v[s], reinterpret_cast<const char*>(A.v) + v_lo,
+                     (uint32_t)(v_hi - v_lo), &sm.full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers --------------------------------
+  const int tid = threadIdx.x;
+  for (int t = 0; t < nt; ++t) {
+    const int s = t % kSpStages;
+    const long long a = R0 + (long long)t * kSpTile;
+    const int nrows = (int)min((long long)kSpTile, R1 - a);
+    mbar_wait(&sm.full[s], (t / kSpStages) & 1);
+    const int base = sm.meta[s][0];
+    const bool staged = sm.meta[s][3] != 0;
+    const int32_t* rps = sm.rp[s];
+    T* ys = sm.ys[t & 1];
+    for (int rr = tid; rr < nrows; rr += kSpConsumers) {
+      const int lo = rps[rr], hi = rps[rr + 1];
+      T y;
+      if (staged) {
+        const int32_t* cs = sm.ci[s] + (lo - base + sm.meta[s][1]);
+        const T* vs = sm.v[s] + (lo - base + sm.meta[s][2]);
+        auto get = [&](int i) -> T { return mul_rn(vs[i], __ldg(x + cs[i])); };
+        y = row_reduce<T>(get, hi - lo);
+      } else {
+        const int32_t* cg = A.ci + lo;
+        const T* vg = A.v + lo;
+        auto get = [&](int i) -> T { return mul_rn(__ldg(vg + i), __ldg(x + __ldg(cg + i))); };
+        y = row_reduce<T>(get, hi - lo);
+      }
+      ys[rr] = epi.on_row(a + rr, y);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sm.empty[s])) : "memory");
+    consumer_sync();
+    epi.on_tile(a, nrows, ys);
+  }
+  epi.on_end();
+}
+
+}  // namespace mpg

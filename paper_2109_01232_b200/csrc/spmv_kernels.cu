@@ -1,0 +1,286 @@
+// SpMV-family kernels: plain SpMV, explicit residual, the fused
+// SpMV + first CGS pass (K_A), and the polynomial-preconditioner steps.
+// All share spmv_pipeline (spmv.cuh); they differ only in the epilogue.
+#include <mutex>
+
+#include "spmv.cuh"
+#include "state.cuh"
+
+namespace mpg {
+
+// Consumer-only last-CTA election (the producer warp has exited).
+__device__ __forceinline__ bool consumers_last_cta(unsigned int* counter, bool* flag) {
+  __threadfence();
+  consumer_sync();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(counter, 1u);
+    *flag = (t == gridDim.x - 1);
+  }
+  consumer_sync();
+  const bool last = *flag;
+  if (last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+  return last;
+}
+
+// Sum columns of partials, consumer warps only.
+template <typename T, typename OutF>
+__device__ __forceinline__ void consumers_finalize(const T* part, int nparts, int stride,
+                                                   int ncols, OutF out) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int c = w; c < ncols; c += kSpConsumerWarps) {
+    T s = T(0);
+    for (int p = l; p < nparts; p += 32) s += __ldcg(part + (size_t)p * stride + c);
+    s = warp_sum(s);
+    if (l == 0) out(c, s);
+  }
+}
+
+// ---------------------------------------------------------------- epilogues
+
+template <typename T>
+struct EpiPlain {
+  T* y;
+  __device__ bool skip() const { return false; }
+  __device__ void init(SpSmem<T>&, unsigned char*) {}
+  __device__ T on_row(long long r, T v) { y[r] = v; return v; }
+  __device__ void on_tile(long long, int, const T*) {}
+  __device__ void on_end() {}
+};
+
+// explicit_residual (solvers.py:443-453): r = b - A x, ||r||
+template <typename T>
+struct EpiResid {
+  const T* b;
+  T* r;
+  double* out;
+  mpg_state_header* hdr;
+  T* part;
+  unsigned int* counter;
+  T ss;
+  SpSmem<T>* sm;
+  __device__ bool skip() const { return false; }
+  __device__ void init(SpSmem<T>& s, unsigned char*) { sm = &s; ss = T(0); }
+  __device__ T on_row(long long i, T y) {
+    const T v = sub_rn(__ldg(b + i), y);
+    r[i] = v;
+    ss = fma_rn(v, v, ss);
+    return v;
+  }
+  __device__ void on_tile(long long, int, const T*) {}
+  __device__ void on_end() {
+    T t = consumer_block_sum(ss, sm->red);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+    __shared__ bool flag;
+    if (consumers_last_cta(counter, &flag)) {
+      consumers_finalize(part, gridDim.x, 1, 1, [&](int, T s) {
+        const double nr = (double)sqrt_rn(s);
+        if (out) *out = nr;
+        if (hdr) hdr->rnorm = nr;
+      });
+    }
+  }
+};
+
+// K_A: w = A x; w0 = ||w||; finite check; c1 = V[:, :k]^T w  (krylov.py:128-139)
+template <typename T>
+struct EpiDot1 {
+  T* w;
+  const T* V;
+  long long ldv;
+  int k;
+  StateView<T> sv;
+  T* part;
+  unsigned int* counter;
+  T ss;
+  int bad;
+  T* acc;
+  SpSmem<T>* sm;
+  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
+  __device__ void init(SpSmem<T>& s, unsigned char* extra) {
+    sm = &s;
+    acc = reinterpret_cast<T*>(extra);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) acc[i] = T(0);
+    ss = T(0);
+    bad = 0;
+  }
+  __device__ T on_row(long long i, T y) {
+    w[i] = y;
+    ss = fma_rn(y, y, ss);
+    bad |= !isfinite(y);
+    return y;
+  }
+  __device__ void on_tile(long long a, int nr, const T* ys) {
+    auto vrow = [&](int i) { return V + (size_t)i * ldv + a; };
+    tile_dots<T, kLoadStream>(k, nr, vrow, ys, acc, sm->acc);
+  }
+  __device__ void on_end() {
+    T t = consumer_block_sum(ss, sm->red);
+    const int stride = k + 2;
+    // publish partials: acc[0..k), ||w||^2, non-finite count
+    consumer_sync();
+    for (int i = threadIdx.x; i < k; i += kSpConsumers) part[(size_t)blockIdx.x * stride + i] = acc[i];
+    const int anybad = __any_sync(0xffffffffu, bad);
+    __shared__ int badw[kSpConsumerWarps];
+    if ((threadIdx.x & 31) == 0) badw[threadIdx.x >> 5] = anybad;
+    consumer_sync();
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
+      part[(size_t)blockIdx.x * stride + k] = t;
+      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
+    }
+    __shared__ bool flag;
+    if (consumers_last_cta(counter, &flag)) {
+      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+        if (c < k) {
+          sv.c1[c] = s;
+        } else if (c == k) {
+          sv.h->w0 = (double)sqrt_rn(s);
+        } else if (s != T(0)) {
+          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
+          sv.h->done = 1;
+        }
+      });
+    }
+  }
+};
+
+// polynomial preconditioner steps (precond.py:272-319); the SpMV input is
+// `x` of the pipeline; other operands are own-row elementwise.
+template <typename T>
+struct EpiPoly {
+  int op;
+  T a, b;
+  const T* src;   // SpMV input (also own-row operand)
+  const T* x2;    // second operand (x for HORNER, p for PAIR2)
+  T* dst;
+  T* y;           // accumulator (NEWTON_REAL, PAIR1)
+  const mpg_state_header* gate;
+  __device__ bool skip() const { return gate && *(volatile const int*)&gate->done != 0; }
+  __device__ void init(SpSmem<T>&, unsigned char*) {}
+  __device__ T on_row(long long i, T v) {
+    switch (op) {
+      case MPG_POLY_HORNER: {  // y = spmv(A, y); y += c[i] * x
+        const T o = add_rn(v, mul_rn(a, x2[i]));
+        dst[i] = o;
+        return o;
+      }
+      case MPG_POLY_NEWTON_REAL: {  // y += inv * prod ; prod = prod - inv * A prod
+        const T p = src[i];
+        y[i] = add_rn(y[i], mul_rn(a, p));
+        const T o = sub_rn(p, mul_rn(a, v));
+        dst[i] = o;
+        return o;
+      }
+      case MPG_POLY_PAIR1: {  // ap = A prod ; y += a*prod - b*ap
+        const T p = src[i];
+        y[i] = add_rn(y[i], sub_rn(mul_rn(a, p), mul_rn(b, v)));
+        dst[i] = v;
+        return v;
+      }
+      case MPG_POLY_PAIR2: {  // prod = prod - a*ap + b*(A ap)
+        const T o = add_rn(sub_rn(x2[i], mul_rn(a, src[i])), mul_rn(b, v));
+        dst[i] = o;
+        return o;
+      }
+      default:
+        dst[i] = v;
+        return v;
+    }
+  }
+  __device__ void on_tile(long long, int, const T*) {}
+  __device__ void on_end() {}
+};
+
+template <typename T, typename E>
+__global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __restrict__ x, E epi) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  if (epi.skip()) return;
+  SpSmem<T>& sm = *reinterpret_cast<SpSmem<T>*>(smraw);
+  epi.init(sm, smraw + sizeof(SpSmem<T>));
+  spmv_pipeline(A, x, epi, sm);
+}
+
+// ----------------------------------------------------------------- launches
+
+template <typename T, typename E>
+static cudaError_t launch_pipeline(const CsrView<T>& A, const T* x, const E& epi, size_t extra,
+                                   WsView, cudaStream_t st) {
+  const size_t smem = sizeof(SpSmem<T>) + extra;
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(k_spmv<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(SpSmem<T>) + (size_t)(kMaxM + 8) * sizeof(T)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<T, E>, kSpThreads, smem);
+    if (occ < 1) occ = 1;
+  });
+  long long tiles = (A.n + kSpTile - 1) / kSpTile;
+  long long G = (long long)num_sms() * occ;
+  if (tiles < G) G = tiles;
+  if (G < 1) G = 1;
+  count_launch();
+  k_spmv<T, E><<<(unsigned)G, kSpThreads, smem, st>>>(A, x, epi);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_spmv(const CsrView<T>& A, const T* x, T* y, WsView ws, cudaStream_t st) {
+  EpiPlain<T> e{y};
+  return launch_pipeline(A, x, e, 0, ws, st);
+}
+
+template <typename T>
+cudaError_t launch_residual(const CsrView<T>& A, const T* b, const T* x, T* r, double* norm_out,
+                            mpg_state_header* hdr, WsView ws, cudaStream_t st) {
+  EpiResid<T> e{};
+  e.b = b; e.r = r; e.out = norm_out; e.hdr = hdr;
+  e.part = static_cast<T*>(ws.part);
+  e.counter = ws.counter;
+  return launch_pipeline(A, x, e, 0, ws, st);
+}
+
+template <typename T>
+cudaError_t launch_spmv_dot1(const CsrView<T>& A, const T* x, T* w, const T* V, long long ldv,
+                             int k, StateView<T> sv, WsView ws, cudaStream_t st) {
+  EpiDot1<T> e{};
+  e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
+  e.part = static_cast<T*>(ws.part);
+  e.counter = ws.counter;
+  return launch_pipeline(A, x, e, (size_t)(k + 8) * sizeof(T), ws, st);
+}
+
+template <typename T>
+cudaError_t launch_poly_op(const CsrView<T>& A, const mpg_poly_op& op, const T* x, T* y, T* t0,
+                           T* t1, T* t2, const mpg_state_header* gate, long long n, WsView ws,
+                           cudaStream_t st) {
+  T* bufs[5] = {const_cast<T*>(x), y, t0, t1, t2};
+  EpiPoly<T> e{};
+  e.op = op.op;
+  e.a = (T)op.a;
+  e.b = (T)op.b;
+  e.src = bufs[op.src];
+  e.dst = bufs[op.dst];
+  e.x2 = bufs[op.x2];
+  e.y = y;
+  e.gate = gate;
+  return launch_pipeline(A, e.src, e, 0, ws, st);
+}
+
+#define INST(T)                                                                                 \
+  template cudaError_t launch_spmv<T>(const CsrView<T>&, const T*, T*, WsView, cudaStream_t);   \
+  template cudaError_t launch_residual<T>(const CsrView<T>&, const T*, const T*, T*, double*,   \
+                                          mpg_state_header*, WsView, cudaStream_t);            \
+  template cudaError_t launch_spmv_dot1<T>(const CsrView<T>&, const T*, T*, const T*, long long, \
+                                           int, StateView<T>, WsView, cudaStream_t);          \
+  template cudaError_t launch_poly_op<T>(const CsrView<T>&, const mpg_poly_op&, const T*, T*,  \
+                                         T*, T*, T*, const mpg_state_header*, long long,       \
+                                         WsView, cudaStream_t);
+INST(float)
+INST(double)
+#undef INST
+
+}  // namespace mpg

@@ -1,0 +1,193 @@
+"""Generate the golden fixtures under tests/golden/ from the REFERENCE itself.
+
+Run in the build container, where the read-only reference exists:
+
+    python tests/golden/make_golden.py            # small + assembly hashes
+    python tests/golden/make_golden.py --cfg2     # + full Laplace3D(150) runs (~35 min)
+
+Nothing on the GPU box reads /root/reference: the tests only read the
+committed JSON/NPZ written here.  The reference is imported read-only from
+``/root/reference/pkg/src`` (mpgmres 0.1.0, numpy 2.3.5, scipy 1.18.1,
+OpenBLAS 0.3.30 SkylakeX, BLAS pinned to one thread by the reference).
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import mpgmres
+    return mpgmres
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def report_dict(rep) -> dict:
+    return {
+        "converged": bool(rep.converged),
+        "total_iters": int(rep.total_iters),
+        "iters_fp32": int(rep.iters_fp32),
+        "iters_fp64": int(rep.iters_fp64),
+        "loss_of_accuracy": bool(rep.loss_of_accuracy),
+        "stalled_at": rep.stalled_at,
+        # explicit residuals at restart boundaries (the per-cycle record)
+        "boundaries": [[int(e.iteration), float(e.implicit), float(e.explicit), e.phase]
+                       for e in rep.residual_history if e.explicit is not None],
+        "history_len": len(rep.residual_history),
+        "x_sha256": sha(rep.x),
+        "x_norm": float(np.linalg.norm(rep.x)),
+        "x_head": [float(v) for v in rep.x[:4]],
+        "total_time_s": float(rep.total_time),
+    }
+
+
+SMALL_RUNS = [
+    # (name, spec, solver, kwargs)
+    ("laplace2d:50/fp64/m50", ("laplace2d", 50, {}), "fp64", {"m": 50}),
+    ("laplace2d:50/ir/m50", ("laplace2d", 50, {}), "ir", {"m": 50}),
+    ("laplace2d:100/fp64/m50", ("laplace2d", 100, {}), "fp64", {"m": 50}),
+    ("laplace2d:100/ir/m50", ("laplace2d", 100, {}), "ir", {"m": 50}),
+    ("laplace2d:100/fd200/m50", ("laplace2d", 100, {}), "fd", {"m": 50, "switch_iter": 200}),
+    ("laplace2d:100/fp64/m25", ("laplace2d", 100, {}), "fp64", {"m": 25}),
+    ("laplace2d:100/ir/m25", ("laplace2d", 100, {}), "ir", {"m": 25}),
+    ("laplace2d:100/fp64/m100", ("laplace2d", 100, {}), "fp64", {"m": 100}),
+    ("laplace2d:100/ir/m100", ("laplace2d", 100, {}), "ir", {"m": 100}),
+    ("laplace2d:100/fp32/m50/max5000", ("laplace2d", 100, {}), "fp32", {"m": 50, "max_iters": 5000}),
+    ("laplace3d:40/fp64/m50", ("laplace3d", 40, {}), "fp64", {"m": 50}),
+    ("laplace3d:40/ir/m50", ("laplace3d", 40, {}), "ir", {"m": 50}),
+    ("laplace3d:30/fd100/m50", ("laplace3d", 30, {}), "fd", {"m": 50, "switch_iter": 100}),
+    ("convdiff2d:100:c100/fp64/m50", ("convdiff2d", 100, {"convection": 100.0}), "fp64", {"m": 50}),
+    ("convdiff2d:100:c100/ir/m50", ("convdiff2d", 100, {"convection": 100.0}), "ir", {"m": 50}),
+    ("convdiff2d:60:c61/ir+jacobi1/m50", ("convdiff2d", 60, {"convection": 61.0}), "ir+jacobi1", {"m": 50}),
+    ("recirc2d:40:c0.5/ir/m50", ("recirc2d", 40, {"convection": 0.5}), "ir", {"m": 50}),
+    ("laplace3d:20/ir+poly5/m50", ("laplace3d", 20, {}), "ir+poly5", {"m": 50}),
+    ("laplace3d:20/ir+poly25/m50", ("laplace3d", 20, {}), "ir+poly25", {"m": 50}),
+    ("laplace3d:20/fp64+poly25_32/m50", ("laplace3d", 20, {}), "fp64+poly25_32", {"m": 50}),
+    ("laplace2d:20/fp64/m10/max15", ("laplace2d", 20, {}), "fp64", {"m": 10, "max_iters": 15}),
+]
+
+CFG2_RUNS = [
+    ("laplace3d:150/fp64/m50", ("laplace3d", 150, {}), "fp64", {"m": 50}),
+    ("laplace3d:150/ir/m50", ("laplace3d", 150, {}), "ir", {"m": 50}),
+]
+
+
+def run_one(mp, spec, solver, kw):
+    kind, nx, sk = spec
+    A = mp.generate(mp.StencilSpec(mp.StencilKind(kind), nx, **sk))
+    b = np.ones(A.n_rows)
+    crit = mp.StopCriteria(rtol=kw.get("rtol", 1e-10), m=kw["m"],
+                           max_iters=kw.get("max_iters", 100_000))
+    if solver == "fp64":
+        return mp.gmres_restarted(A, b, criteria=crit)
+    if solver == "fp32":
+        return mp.gmres_restarted(A, b, criteria=crit, precision=mp.FP32)
+    if solver == "ir":
+        return mp.gmres_ir(A, b, criteria=crit)
+    if solver == "fd":
+        return mp.gmres_fd(A, b, criteria=crit, switch_iter=kw["switch_iter"])
+    A32 = mp.convert_matrix(A, mp.FP32)
+    if solver == "ir+jacobi1":
+        return mp.gmres_ir(A, b, criteria=crit, precond_fp32=mp.build_block_jacobi(A32, 1))
+    if solver.startswith("ir+poly"):
+        M = mp.build_poly_precond(A32, int(solver[7:]), seed=0)
+        return mp.gmres_ir(A, b, criteria=crit, precond_fp32=M)
+    if solver == "fp64+poly25_32":
+        M = mp.build_poly_precond(A32, 25, seed=0)
+        return mp.gmres_restarted(A, b, criteria=crit, precond=M)
+    raise ValueError(solver)
+
+
+ASSEMBLY = [  # (kind, nx, kwargs): sha256 of row_ptr / col_idx / values
+    ("laplace2d", 100, {}),
+    ("laplace3d", 150, {}),
+    ("convdiff2d", 1500, {"convection": 1501.0}),
+    ("recirc2d", 1500, {"convection": 1.0}),
+    ("laplace3d", 200, {}),
+    ("recirc2d", 77, {"convection": 40.1}),
+    ("stretched2d", 60, {}),
+    ("biharmonic2d", 33, {}),
+    ("star2d", 31, {}),
+]
+
+
+def spmv_fixtures(mp):
+    """Small SpMV cases: matrices, x, and the reference's y, both precisions."""
+    rng = np.random.default_rng(20260101)
+    out = {}
+    cases = [("laplace3d", 7, {}), ("laplace2d", 17, {}), ("convdiff2d", 15, {"convection": 1501.0}),
+             ("recirc2d", 19, {"convection": 40.1}), ("biharmonic2d", 14, {}), ("star2d", 16, {})]
+    mats = [(f"{k}:{nx}", mp.generate(mp.StencilSpec(mp.StencilKind(k), nx, **kw)))
+            for k, nx, kw in cases]
+    # long rows (numpy pairwise sum with 8-way unrolling and recursive split)
+    for n, dens in ((64, 0.5), (300, 0.6)):
+        d = rng.standard_normal((n, n)) * (rng.random((n, n)) < dens)
+        d[5, :] = 0.0  # an empty row
+        mats.append((f"dense{n}", mp.CsrMatrix.from_dense(d)))
+    for name, A in mats:
+        for prec in ("fp64", "fp32"):
+            Ap = A if prec == "fp64" else mp.convert_matrix(A, mp.FP32)
+            x = rng.standard_normal(A.n_cols).astype(Ap.values.dtype)
+            y = mp.spmv(Ap, x)
+            key = f"{name}/{prec}"
+            out[key + "/row_ptr"] = Ap.row_ptr
+            out[key + "/col_idx"] = Ap.col_idx
+            out[key + "/values"] = Ap.values
+            out[key + "/x"] = x
+            out[key + "/y"] = y
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--skip-small", action="store_true")
+    args = ap.parse_args()
+    mp = _ref()
+    meta = {"reference": "mpgmres " + mp.__version__, "numpy": np.__version__,
+            "generated": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    if not args.skip_small:
+        runs = {}
+        for name, spec, solver, kw in SMALL_RUNS:
+            t = time.time()
+            runs[name] = report_dict(run_one(mp, spec, solver, kw))
+            print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
+        with open(os.path.join(HERE, "reference_runs.json"), "w") as f:
+            json.dump({"meta": meta, "runs": runs}, f, indent=1)
+        asm = {}
+        for kind, nx, kw in ASSEMBLY:
+            A = mp.generate(mp.StencilSpec(mp.StencilKind(kind), nx, **kw))
+            asm[f"{kind}:{nx}:" + ",".join(f"{k}={v}" for k, v in kw.items())] = {
+                "kind": kind, "nx": nx, "kwargs": kw, "n": A.n_rows, "nnz": A.nnz,
+                "row_ptr": sha(A.row_ptr), "col_idx": sha(A.col_idx), "values": sha(A.values)}
+            print("assembly", kind, nx, flush=True)
+            del A
+        with open(os.path.join(HERE, "assembly_sha256.json"), "w") as f:
+            json.dump({"meta": meta, "matrices": asm}, f, indent=1)
+        np.savez_compressed(os.path.join(HERE, "spmv_cases.npz"), **spmv_fixtures(mp))
+    if args.cfg2:
+        runs = {}
+        for name, spec, solver, kw in CFG2_RUNS:
+            t = time.time()
+            runs[name] = report_dict(run_one(mp, spec, solver, kw))
+            print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
+        with open(os.path.join(HERE, "reference_cfg2.json"), "w") as f:
+            json.dump({"meta": meta, "runs": runs}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

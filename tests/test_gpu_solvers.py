@@ -1,0 +1,219 @@
+"""GPU solver parity against the reference (via its recorded fixtures) and the
+oracle, at sizes the oracle finishes in seconds.
+
+North-star bars (BASELINE.json): iteration counts within +-2 % of the CPU
+reference for the same solver, final fp64 relative residual <= rtol, and the
+solution within 1e-8 relative of the reference's.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2109_01232_b200 as P
+from oracle import cpu_gmres as O
+from paper_2109_01232_b200 import _lib
+
+
+def dev(Ao):
+    return P.CsrMatrix(Ao.n_rows, Ao.n_cols, Ao.row_ptr, Ao.col_idx, Ao.values)
+
+
+def within_2pct(got, want):
+    return abs(got - want) <= max(0.02 * want, 0)
+
+
+def rel_err(x, y):
+    return float(np.linalg.norm(np.asarray(x) - np.asarray(y)) / np.linalg.norm(np.asarray(y)))
+
+
+SOLVER_CASES = [
+    # name, kind, nx, kwargs, solver, extra
+    ("laplace2d:50/fp64/m50", "laplace2d", 50, {}, "fp64", {"m": 50}),
+    ("laplace2d:50/ir/m50", "laplace2d", 50, {}, "ir", {"m": 50}),
+    ("laplace2d:100/fp64/m50", "laplace2d", 100, {}, "fp64", {"m": 50}),
+    ("laplace2d:100/ir/m50", "laplace2d", 100, {}, "ir", {"m": 50}),
+    ("laplace2d:100/fd200/m50", "laplace2d", 100, {}, "fd", {"m": 50, "switch_iter": 200}),
+    ("laplace2d:100/fp64/m25", "laplace2d", 100, {}, "fp64", {"m": 25}),
+    ("laplace2d:100/ir/m25", "laplace2d", 100, {}, "ir", {"m": 25}),
+    ("laplace2d:100/fp64/m100", "laplace2d", 100, {}, "fp64", {"m": 100}),
+    ("laplace2d:100/ir/m100", "laplace2d", 100, {}, "ir", {"m": 100}),
+    ("laplace3d:40/fp64/m50", "laplace3d", 40, {}, "fp64", {"m": 50}),
+    ("laplace3d:30/fd100/m50", "laplace3d", 30, {}, "fd", {"m": 50, "switch_iter": 100}),
+    ("convdiff2d:100:c100/fp64/m50", "convdiff2d", 100, {"convection": 100.0}, "fp64", {"m": 50}),
+    ("convdiff2d:100:c100/ir/m50", "convdiff2d", 100, {"convection": 100.0}, "ir", {"m": 50}),
+    ("recirc2d:40:c0.5/ir/m50", "recirc2d", 40, {"convection": 0.5}, "ir", {"m": 50}),
+]
+
+
+def run(A, b, solver, extra):
+    crit = P.StopCriteria(rtol=1e-10, m=extra["m"], max_iters=extra.get("max_iters", 100_000))
+    if solver == "fp64":
+        return P.gmres_restarted(A, b, criteria=crit)
+    if solver == "fp32":
+        return P.gmres_restarted(A, b, criteria=crit, precision=P.FP32)
+    if solver == "ir":
+        return P.gmres_ir(A, b, criteria=crit)
+    if solver == "fd":
+        return P.gmres_fd(A, b, criteria=crit, switch_iter=extra["switch_iter"])
+    raise ValueError(solver)
+
+
+def oracle_run(Ao, b, solver, extra):
+    m, mi = extra["m"], extra.get("max_iters", 100_000)
+    if solver == "fp64":
+        return O.solve_restarted(Ao, b, m=m, max_iters=mi)
+    if solver == "fp32":
+        return O.solve_restarted(Ao, b, m=m, max_iters=mi, dtype=np.float32)
+    if solver == "ir":
+        return O.solve_ir(Ao, b, m=m, max_iters=mi)
+    return O.solve_fd(Ao, b, m=m, max_iters=mi, switch_iter=extra["switch_iter"])
+
+
+@pytest.mark.parametrize("case", SOLVER_CASES, ids=[c[0] for c in SOLVER_CASES])
+def test_solver_parity(case, golden_runs):
+    name, kind, nx, kw, solver, extra = case
+    Ao = O.stencil_csr(kind, nx, **kw)
+    b = O.ones_rhs(Ao.n_rows)
+    rep = run(dev(Ao), b, solver, extra)
+    g = golden_runs[name]
+    assert rep.converged == g["converged"]
+    assert within_2pct(rep.total_iters, g["total_iters"]), (rep.total_iters, g["total_iters"])
+    orep = oracle_run(Ao, b, solver, extra)
+    assert orep.total_iters == g["total_iters"]          # oracle pinned to the reference
+    assert rel_err(rep.x, orep.x) <= 1e-8
+    rn, _ = O.residual(Ao, b, np.asarray(rep.x))
+    assert rn / np.linalg.norm(b) <= 1e-10
+    assert isinstance(rep.x, np.ndarray) and rep.x.dtype == np.float64
+    assert len(rep.residual_history) >= 2
+    assert rep.iters_fp32 + rep.iters_fp64 == rep.total_iters
+    assert set(rep.kernel_times) == {"SpMV", "GemvTrans", "Norm", "GemvNoTrans", "Other"}
+
+
+def test_golden_235_and_determinism():
+    Ao = O.stencil_csr("laplace2d", 50)
+    A = dev(Ao)
+    b = np.ones(Ao.n_rows)
+    crit = P.StopCriteria(rtol=1e-10, m=50)
+    r1 = P.gmres_restarted(A, b, criteria=crit)
+    r2 = P.gmres_restarted(A, b, criteria=crit)
+    assert r1.total_iters == 235                 # tests/test_solvers.py:16 GOLDEN_LAPLACE2D50_ITERS
+    assert np.array_equal(r1.x, r2.x)            # bitwise reproducible (fixed-order reductions)
+    assert r1.residual_history == r2.residual_history
+    r3 = P.gmres_restarted(A, b, criteria=crit, use_graph=False)   # eager launches, same bits
+    assert np.array_equal(r1.x, r3.x)
+
+
+def test_device_inputs_stay_on_device():
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE2D, 40))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    rep = P.gmres_ir(A, b, criteria=P.StopCriteria(m=30))
+    assert isinstance(rep.x, torch.Tensor) and rep.x.is_cuda
+    assert rep.converged
+    nr, _ = P.explicit_residual(A, b, rep.x)
+    assert nr / float(torch.linalg.norm(b)) <= 1e-10
+
+
+def test_ir_boundaries_and_fd_switch_zero():
+    Ao = O.stencil_csr("laplace2d", 40)
+    A, b = dev(Ao), np.ones(Ao.n_rows)
+    crit = P.StopCriteria(rtol=1e-10, m=30)
+    rep = P.gmres_ir(A, b, criteria=crit)
+    marks = [e.iteration for e in rep.residual_history if e.explicit is not None]
+    assert rep.total_iters in marks
+    fd = P.gmres_fd(A, b, criteria=P.StopCriteria(m=50), switch_iter=0)
+    dbl = P.gmres_restarted(A, b, criteria=P.StopCriteria(m=50))
+    assert fd.total_iters == dbl.total_iters and np.array_equal(fd.x, dbl.x)
+    assert fd.residual_history == dbl.residual_history
+    fd = P.gmres_fd(A, b, criteria=P.StopCriteria(m=25), switch_iter=50)
+    phases = [e.phase for e in fd.residual_history]
+    assert sum(1 for a, c in zip(phases, phases[1:]) if a != c) == 1
+    with pytest.raises(ValueError):
+        P.gmres_fd(A, b, criteria=P.StopCriteria(m=50), switch_iter=75)
+
+
+def test_fp32_plateau_and_stall(golden_runs):
+    Ao = O.stencil_csr("laplace2d", 100)
+    rep = P.gmres_restarted(dev(Ao), np.ones(Ao.n_rows), precision=P.FP32,
+                            criteria=P.StopCriteria(rtol=1e-10, m=50, max_iters=5000))
+    g = golden_runs["laplace2d:100/fp32/m50/max5000"]
+    assert not rep.converged and rep.total_iters == 5000
+    assert 1e-8 <= rep.best_explicit() <= 1e-4
+    assert rep.x.dtype == np.float64
+    assert rep.stalled_at is not None and g["stalled_at"] is not None
+    Ao = O.stencil_csr("laplace2d", 20)
+    rep = P.gmres_restarted(dev(Ao), np.ones(Ao.n_rows), criteria=P.StopCriteria(m=10, max_iters=15))
+    assert not rep.converged and rep.total_iters == 15
+
+
+def test_small_exact_cases():
+    A = P.CsrMatrix.from_dense(np.eye(37))
+    b = np.random.default_rng(3).standard_normal(37)
+    rep = P.gmres_restarted(A, b)
+    assert rep.converged and rep.total_iters == 1 and np.allclose(rep.x, b, atol=1e-12)
+    A = P.CsrMatrix.from_dense(np.array([[4.0, 1.0], [1.0, 3.0]]))
+    res = P.gmres_cycle(lambda v: P.spmv(A, v), np.array([1.0, 2.0]), np.zeros(2), 2, 1e-12)
+    assert np.abs(res.x - [1.0 / 11.0, 7.0 / 11.0]).max() <= 1e-10
+    A = P.CsrMatrix.from_dense(np.eye(8))
+    b = np.zeros(8); b[0] = 2.5
+    rep = P.gmres_ir(A, b)
+    assert rep.converged and rep.iters_fp32 == 1
+    with pytest.raises(P.PrecisionError):
+        P.gmres_ir(P.convert_matrix(P.CsrMatrix.from_dense(np.eye(4)), P.FP32), np.ones(4))
+
+
+def test_gmres_cycle_generic_operator_matches_oracle(rng):
+    Ao = O.stencil_csr("convdiff2d", 30, convection=20.0)
+    A = dev(Ao)
+    b = rng.standard_normal(Ao.n_rows)
+    cy = P.gmres_cycle(lambda v: P.spmv(A, v), b, np.zeros_like(b), 40, 1e-300)
+    co = O.cycle(lambda v: O.spmv(Ao, v), b, np.zeros_like(b), 40, 1e-300)
+    assert cy.steps == co.steps == 40
+    assert np.allclose(cy.implicit_norms, co.implicit, rtol=1e-8)
+    assert rel_err(cy.x, co.x) <= 1e-8
+
+
+def test_ir_with_oracle_jacobi_and_poly(golden_runs):
+    Ao = O.stencil_csr("convdiff2d", 60, convection=61.0)
+    A, b = dev(Ao), np.ones(Ao.n_rows)
+    Mo = O.jacobi_build(Ao.astype(np.float32), 1)
+    rep = P.gmres_ir(A, b, precond_fp32=Mo)
+    g = golden_runs["convdiff2d:60:c61/ir+jacobi1/m50"]
+    assert rep.converged and within_2pct(rep.total_iters, g["total_iters"])
+    Mdev = P.build_block_jacobi(P.convert_matrix(A, P.FP32), 1)
+    rep2 = P.gmres_ir(A, b, precond_fp32=Mdev)
+    assert rep2.total_iters == rep.total_iters and np.array_equal(rep2.x, rep.x)
+    rep3 = P.gmres_ir(A, b, precond_fp32=P.build_block_jacobi(P.convert_matrix(A, P.FP32), 4))
+    assert rep3.converged
+
+    Ao = O.stencil_csr("laplace3d", 20)
+    A, b = dev(Ao), np.ones(Ao.n_rows)
+    for deg, key in ((5, "laplace3d:20/ir+poly5/m50"), (25, "laplace3d:20/ir+poly25/m50")):
+        Mo = O.poly_build(Ao.astype(np.float32), deg, seed=0)
+        rep = P.gmres_ir(A, b, precond_fp32=Mo)
+        g = golden_runs[key]
+        assert rep.converged
+        assert abs(rep.total_iters - g["total_iters"]) <= max(1, int(0.02 * g["total_iters"])), (deg, rep.total_iters)
+        orep = O.solve_ir(Ao, b, precond32=Mo)
+        assert rel_err(rep.x, orep.x) <= 1e-8
+    # fp32 polynomial inside an fp64 solve: cast_apply path, false convergence flagged
+    Mo = O.poly_build(Ao.astype(np.float32), 25, seed=0)
+    rep = P.gmres_restarted(A, b, precond=Mo)
+    assert rep.loss_of_accuracy == golden_runs["laplace3d:20/fp64+poly25_32/m50"]["loss_of_accuracy"]
+
+
+def test_divergence_is_raised():
+    d = np.eye(4)
+    d[2, 2] = np.inf
+    A = P.CsrMatrix.from_dense(d)
+    with pytest.raises(P.DivergenceError):
+        P.gmres_restarted(A, np.ones(4))
+
+
+def test_native_code_launched():
+    before = _lib.launch_count()
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE2D, 30))
+    P.gmres_ir(A, np.ones(A.n_rows))
+    assert _lib.launch_count() - before > 100
