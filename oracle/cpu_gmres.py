@@ -585,8 +585,8 @@ class Jacobi(NamedTuple):
     block_size: int
     n: int
     dtype: np.dtype
-    lu: np.ndarray             # (nb, k, k)
-    piv: np.ndarray            # (nb, k)
+    block_lu: np.ndarray             # (nb, k, k)
+    block_piv: np.ndarray            # (nb, k)
 
 
 def poly_build(A: Csr, degree: int, seed: int = 0, threads=_BLAS_THREADS) -> Poly:
@@ -735,19 +735,19 @@ def jacobi_build(A: Csr, block_size: int) -> Jacobi:
 
 def jacobi_apply(M: Jacobi, x: np.ndarray) -> np.ndarray:
     """Batched block LU solves (precond.py:363-390)."""
-    nb, k = M.lu.shape[:2]
+    nb, k = M.block_lu.shape[:2]
     xb = np.zeros((nb, k), dtype=x.dtype)
     xb.reshape(-1)[: M.n] = x
     rr = np.arange(nb)
     for i in range(k):
-        j = M.piv[:, i]
+        j = M.block_piv[:, i]
         vi = xb[rr, i].copy()
         xb[rr, i] = xb[rr, j]
         xb[rr, j] = vi
     for i in range(1, k):
-        xb[:, i] -= np.einsum("bt,bt->b", M.lu[:, i, :i], xb[:, :i])
+        xb[:, i] -= np.einsum("bt,bt->b", M.block_lu[:, i, :i], xb[:, :i])
     for i in range(k - 1, -1, -1):
         if i < k - 1:
-            xb[:, i] -= np.einsum("bt,bt->b", M.lu[:, i, i + 1:], xb[:, i + 1:])
-        xb[:, i] /= M.lu[:, i, i]
+            xb[:, i] -= np.einsum("bt,bt->b", M.block_lu[:, i, i + 1:], xb[:, i + 1:])
+        xb[:, i] /= M.block_lu[:, i, i]
     return xb.reshape(-1)[: M.n].copy()

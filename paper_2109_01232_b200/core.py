@@ -436,7 +436,11 @@ def gemv(a, x, y=None, *, alpha: float = 1.0, beta: float = 0.0, transpose: bool
             return z if host else torch.zeros(out_len, dtype=prec.torch_dtype, device=device())
         y *= beta
         return y
-    ad = to_device(a) if host else a
+    if host:
+        # keep Fortran-ordered multivectors column-major on the device
+        ad = to_device(a.T).t() if (a.flags.f_contiguous and not a.flags.c_contiguous) else to_device(a)
+    else:
+        ad = a
     # express as `nvec` vectors of length `vlen` at stride lda (column-major)
     if ad.stride(0) == 1 and ad.stride(1) >= rows:
         base, vlen, nvec, lda, tr = ad, rows, cols, ad.stride(1), transpose
@@ -445,6 +449,12 @@ def gemv(a, x, y=None, *, alpha: float = 1.0, beta: float = 0.0, transpose: bool
     else:
         ad = ad.t().contiguous().t()
         base, vlen, nvec, lda, tr = ad, rows, cols, ad.stride(1), transpose
+    if tr and nvec > 512 and cols <= 512:
+        # the multi-dot kernel handles <= 512 vectors: re-lay the matrix column-major
+        ad = ad.t().contiguous().t()
+        base, vlen, nvec, lda, tr = ad, rows, cols, ad.stride(1), transpose
+    if tr and nvec > 512:
+        raise ShapeError("transposed gemv supports at most 512 vectors")
     xd = to_device(x)
     yd = torch.zeros(out_len, dtype=prec.torch_dtype, device=device()) if y is None else to_device(y)
     t0 = timing.tick()

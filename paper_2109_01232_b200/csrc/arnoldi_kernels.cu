@@ -201,7 +201,7 @@ __device__ double hypot_kernel(double ax, double ay) {
   double t1, t2;
   if (h <= 2.0 * ay) {
     const double delta = h - ay;
-    t1 = ax * (ax - 2.0 * delta);
+    t1 = ax * (2.0 * delta - ax);
     t2 = (delta - 2.0 * (ax - ay)) * delta;
   } else {
     const double delta = h - ax;
@@ -592,7 +592,8 @@ cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* 
                               StateView<T> sv, WsView ws, cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(k_update_dot<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_update_dot<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaGetLastError();
   });
   const size_t sz = sizeof(T);
   const size_t budget = 200 * 1024;

@@ -216,6 +216,7 @@ static cudaError_t launch_pipeline(const CsrView<T>& A, const T* x, const E& epi
     cudaFuncSetAttribute(k_spmv<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(SpSmem<T>) + (size_t)(kMaxM + 8) * sizeof(T)));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv<T, E>, kSpThreads, smem);
+    cudaGetLastError();
     if (occ < 1) occ = 1;
   });
   long long tiles = (A.n + kSpTile - 1) / kSpTile;

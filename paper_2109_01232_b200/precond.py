@@ -95,6 +95,8 @@ def precision_of(M) -> Precision:
     p = getattr(M, "precision", None)
     if isinstance(p, Precision):
         return p
+    if p is None and hasattr(M, "dtype"):       # oracle objects carry a numpy dtype
+        return Precision.of(np.zeros(0, dtype=M.dtype))
     val = getattr(p, "value", p)
     if val == "fp32":
         return FP32

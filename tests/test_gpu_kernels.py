@@ -155,8 +155,8 @@ def test_jacobi_build_and_apply(rng):
     for k in (1, 3, 4, 7):
         Mo = O.jacobi_build(A32o, k)
         M = P.build_block_jacobi(A32, k)
-        assert np.array_equal(M.block_piv.cpu().numpy(), Mo.piv)
-        assert np.allclose(M.block_lu.cpu().numpy(), Mo.lu, rtol=1e-5, atol=1e-6)
+        assert np.array_equal(M.block_piv.cpu().numpy(), Mo.block_piv)
+        assert np.allclose(M.block_lu.cpu().numpy(), Mo.block_lu, rtol=1e-5, atol=1e-6)
         y = P.apply_block_jacobi(Mo, x)       # oracle factors, device apply
         yo = O.jacobi_apply(Mo, x)
         if k == 1:
@@ -182,11 +182,11 @@ def test_poly_apply_matches_oracle(degree, rng):
 def test_poly_build_on_device_close_to_oracle():
     Ao = O.stencil_csr("laplace2d", 20)
     A = P.CsrMatrix(Ao.n_rows, Ao.n_cols, Ao.row_ptr, Ao.col_idx, Ao.values)
-    M = P.build_poly_precond(A, 5, seed=0)
-    Mo = O.poly_build(Ao, 5, seed=0)
-    assert M.basis is P.PolyBasis.POWER
-    assert np.allclose(M.coefficients, Mo.coefficients, rtol=1e-8)
-    M = P.build_poly_precond(A, 15, seed=0)
-    Mo = O.poly_build(Ao, 15, seed=0)
-    assert M.basis is P.PolyBasis.NEWTON_ROOTS
-    assert np.allclose(np.sort_complex(M.roots), np.sort_complex(Mo.roots), rtol=1e-6)
+    x = np.random.default_rng(5).standard_normal(Ao.n_rows)
+    for deg, basis in ((5, P.PolyBasis.POWER), (15, P.PolyBasis.NEWTON_ROOTS)):
+        M = P.build_poly_precond(A, deg, seed=0)
+        Mo = O.poly_build(Ao, deg, seed=0)
+        assert M.basis is basis and M.degree == Mo.degree == deg
+        # same polynomial up to the (different) reduction order of the build's dots
+        y, yo = P.apply_poly(M, A, x), O.poly_apply(Mo, Ao, x)
+        assert np.linalg.norm(y - yo) <= 1e-7 * np.linalg.norm(yo)
