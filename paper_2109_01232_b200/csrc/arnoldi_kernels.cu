@@ -135,6 +135,82 @@ __global__ void __launch_bounds__(kUdThreads) k_update_dot(const T* __restrict__
   }
 }
 
+// ===================================== K_B, register variant (k <= KT <= 64)
+// Thread-per-row: the k basis values of a row are loaded once into
+// registers, used for w' = w - V c1 and then for the c2 accumulators
+// (KT per thread), so V streams from HBM exactly once with coalesced loads
+// and no shared-memory staging.  One CTA-level reduction at the end.
+template <typename T, int KT>
+__global__ void __launch_bounds__(kThreads) k_update_dot_reg(const T* __restrict__ V, long long ldv,
+                                                             long long n, int k, T* __restrict__ w,
+                                                             StateView<T> sv, WsView ws) {
+  if (gated(sv.h)) return;
+  constexpr int ROWS = KT <= 4 ? 4 : (KT <= 8 ? 2 : 1);
+  __shared__ T c1s[KT];
+  __shared__ T red2[kWarps][KT];
+  __shared__ bool lastflag;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < KT) c1s[tid] = tid < k ? sv.c1[tid] : T(0);
+  __syncthreads();
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  T acc[KT];
+#pragma unroll
+  for (int i = 0; i < KT; ++i) acc[i] = T(0);
+  for (long long rb = R0 + tid; rb < R1; rb += (long long)kThreads * ROWS) {
+    T v[ROWS][KT];
+    T wv[ROWS];
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) {
+      const long long r = rb + (long long)q * kThreads;
+      const bool ok = r < R1;
+      wv[q] = ok ? w[r] : T(0);
+#pragma unroll
+      for (int i = 0; i < KT; ++i) v[q][i] = (ok && i < k) ? __ldcs(V + (size_t)i * ldv + r) : T(0);
+    }
+#pragma unroll
+    for (int q = 0; q < ROWS; ++q) {
+      const long long r = rb + (long long)q * kThreads;
+      T u = T(0);
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+        if (i < k) u = fma_rn(v[q][i], c1s[i], u);
+      const T x = sub_rn(wv[q], u);
+      if (r < R1) w[r] = x;
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+        if (i < k) acc[i] = fma_rn(v[q][i], x, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < KT; ++i) {
+    if (i < k) {
+      const T a = warp_sum(acc[i]);
+      if (lane == 0) red2[warp][i] = a;
+    }
+  }
+  __syncthreads();
+  T* part = static_cast<T*>(ws.part);
+  if (tid < k) {
+    T s = T(0);
+    for (int q = 0; q < kWarps; ++q) s += red2[q][tid];
+    part[(size_t)blockIdx.x * k + tid] = s;
+  }
+  if (last_cta(ws.counter)) {
+    const int j = k - 1;
+    for (int c = warp; c < k; c += kWarps) {
+      T s2 = T(0);
+      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        sv.c2[c] = s2;
+        sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
+      }
+    }
+  }
+  (void)lastflag;
+}
+
 // ================================== generic-operator pass-1 dots (no SpMV)
 // c1 = V[:, :k]^T w, w0 = ||w||, finite check (krylov.py:133-139) for a w
 // produced by an arbitrary operator.
@@ -588,8 +664,48 @@ cudaError_t launch_dot1_w(const T* w, long long n, const T* V, long long ldv, in
 }
 
 template <typename T>
+cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,
+                                  StateView<T> sv, WsView ws, cudaStream_t st);
+
+template <typename T, int KT>
+static cudaError_t launch_update_dot_reg(const T* V, long long ldv, long long n, int k, T* w,
+                                         StateView<T> sv, WsView ws, cudaStream_t st) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [] {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dot_reg<T, KT>, kThreads, 0);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  long long G = (n + kThreads - 1) / kThreads;
+  const long long cap = (long long)num_sms() * occ;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_update_dot_reg<T, KT><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
+  return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* w,
                               StateView<T> sv, WsView ws, cudaStream_t st) {
+  if (k <= 2) return launch_update_dot_reg<T, 2>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 4) return launch_update_dot_reg<T, 4>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 8) return launch_update_dot_reg<T, 8>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 12) return launch_update_dot_reg<T, 12>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 16) return launch_update_dot_reg<T, 16>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 24) return launch_update_dot_reg<T, 24>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 32) return launch_update_dot_reg<T, 32>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 40) return launch_update_dot_reg<T, 40>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 48) return launch_update_dot_reg<T, 48>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 56) return launch_update_dot_reg<T, 56>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 64) return launch_update_dot_reg<T, 64>(V, ldv, n, k, w, sv, ws, st);
+  return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
+}
+
+template <typename T>
+cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,
+                                  StateView<T> sv, WsView ws, cudaStream_t st) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(k_update_dot<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);

@@ -180,8 +180,57 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // where pairwise is numpy's pairwise_sum: sequential from -0.0 below 8 terms,
 // 8 interleaved accumulators up to 128, recursive halving above.
 
+// 8 <= n <= 128: eight interleaved accumulators, tree, sequential remainder
 template <typename T, typename Get>
-__device__ __noinline__ T pairwise_long(const Get& get, int i0, int n);
+__device__ __forceinline__ T pairwise_block(const Get& get, int i0, int n) {
+  T r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = get(i0 + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], get(i0 + i + j));
+  }
+  T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])),
+                 add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
+  for (; i < n; ++i) res = add_rn(res, get(i0 + i));
+  return res;
+}
+
+// numpy's recursive halving (n2 = n/2 rounded down to a multiple of 8) for
+// n > 128, evaluated post-order with an explicit stack: no device-side call,
+// so the common short-row path keeps every register.
+template <typename T, typename Get>
+__device__ __forceinline__ T pairwise_split(const Get& get, int i0, int n) {
+  int si[32], sn[32], ss[32];
+  T sv[32];
+  int sp = 0;
+  si[0] = i0; sn[0] = n; ss[0] = 0;
+  T ret = T(0);
+  while (sp >= 0) {
+    const int cn = sn[sp];
+    if (cn <= 128) {
+      ret = pairwise_block<T>(get, si[sp], cn);
+      --sp;
+      continue;
+    }
+    const int n2 = cn / 2 - (cn / 2) % 8;
+    if (ss[sp] == 0) {
+      ss[sp] = 1;
+      si[sp + 1] = si[sp]; sn[sp + 1] = n2; ss[sp + 1] = 0;
+      ++sp;
+    } else if (ss[sp] == 1) {
+      sv[sp] = ret;
+      ss[sp] = 2;
+      si[sp + 1] = si[sp] + n2; sn[sp + 1] = cn - n2; ss[sp + 1] = 0;
+      ++sp;
+    } else {
+      ret = add_rn(sv[sp], ret);
+      --sp;
+    }
+  }
+  return ret;
+}
 
 template <typename T, typename Get>
 __device__ __forceinline__ T pairwise(const Get& get, int i0, int n) {
@@ -190,30 +239,8 @@ __device__ __forceinline__ T pairwise(const Get& get, int i0, int n) {
     for (int i = 0; i < n; ++i) r = add_rn(r, get(i0 + i));
     return r;
   }
-  return pairwise_long<T>(get, i0, n);
-}
-
-template <typename T, typename Get>
-__device__ __noinline__ T pairwise_long(const Get& get, int i0, int n) {
-  if (n <= 128) {
-    T r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = get(i0 + j);
-    int i = 8;
-    for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], get(i0 + i + j));
-    }
-    T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])),
-                   add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
-    for (; i < n; ++i) res = add_rn(res, get(i0 + i));
-    return res;
-  }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  T a = pairwise_long<T>(get, i0, n2);
-  T b = (n - n2 < 8) ? pairwise<T>(get, i0 + n2, n - n2) : pairwise_long<T>(get, i0 + n2, n - n2);
-  return add_rn(a, b);
+  if (n <= 128) return pairwise_block<T>(get, i0, n);
+  return pairwise_split<T>(get, i0, n);
 }
 
 template <typename T, typename Get>

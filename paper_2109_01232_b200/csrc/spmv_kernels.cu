@@ -2,6 +2,7 @@
 // SpMV + first CGS pass (K_A), and the polynomial-preconditioner steps.
 // All share spmv_pipeline (spmv.cuh); they differ only in the epilogue.
 #include <mutex>
+#include <type_traits>
 
 #include "spmv.cuh"
 #include "state.cuh"
@@ -148,6 +149,111 @@ struct EpiDot1 {
   }
 };
 
+// K_A, register variant for k <= KT: the thread that computes w_r also
+// accumulates V[i][r] * w_r into KT per-thread accumulators (coalesced
+// across the warp), so the pass-1 dots need no shared-memory tile phase.
+// One CTA-level reduction of the accumulators at the end.
+template <typename T, int KT>
+struct EpiDot1Reg {
+  T* w;
+  const T* V;
+  long long ldv;
+  int k;
+  StateView<T> sv;
+  T* part;
+  unsigned int* counter;
+  T ss;
+  int bad;
+  T acc[KT];
+  T* red2;   // [kSpConsumerWarps][KT] in dynamic smem
+  SpSmem<T>* sm;
+  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
+  __device__ void init(SpSmem<T>& s, unsigned char* extra) {
+    sm = &s;
+    red2 = reinterpret_cast<T*>(extra);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) acc[i] = T(0);
+    ss = T(0);
+    bad = 0;
+  }
+  __device__ T on_row(long long r, T y) {
+    w[r] = y;
+    ss = fma_rn(y, y, ss);
+    bad |= !isfinite(y);
+    return y;
+  }
+  // After the tile's w is complete in shared memory: thread t owns tile rows
+  // [2t, 2t+2) and streams that 2-row slice of every basis vector with
+  // back-to-back 8/16-byte loads (k independent loads in flight per thread).
+  __device__ void on_tile(long long a, int nr, const T* ys) {
+    const int rr = 2 * (int)threadIdx.x;
+    if (rr + 1 < nr) {
+      const T y0 = ys[rr], y1 = ys[rr + 1];
+      const T* v = V + a + rr;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        if (i < k) {
+          T q0, q1;
+          if constexpr (sizeof(T) == 4) {
+            const float2 q = __ldcs(reinterpret_cast<const float2*>(v + (size_t)i * ldv));
+            q0 = q.x; q1 = q.y;
+          } else {
+            const double2 q = __ldcs(reinterpret_cast<const double2*>(v + (size_t)i * ldv));
+            q0 = q.x; q1 = q.y;
+          }
+          acc[i] = fma_rn(q1, y1, fma_rn(q0, y0, acc[i]));
+        }
+      }
+    } else if (rr < nr) {
+      const T y0 = ys[rr];
+      const T* v = V + a + rr;
+#pragma unroll
+      for (int i = 0; i < KT; ++i)
+        if (i < k) acc[i] = fma_rn(__ldcs(v + (size_t)i * ldv), y0, acc[i]);
+    }
+  }
+  __device__ void on_end() {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T t = consumer_block_sum(ss, sm->red);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+      if (i < k) {
+        const T a = warp_sum(acc[i]);
+        if (lane == 0) red2[warp * KT + i] = a;
+      }
+    }
+    const int anybad = __any_sync(0xffffffffu, bad);
+    __shared__ int badw[kSpConsumerWarps];
+    if (lane == 0) badw[warp] = anybad;
+    consumer_sync();
+    const int stride = k + 2;
+    if ((int)threadIdx.x < k) {
+      T s = T(0);
+      for (int q = 0; q < kSpConsumerWarps; ++q) s += red2[q * KT + threadIdx.x];
+      part[(size_t)blockIdx.x * stride + threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
+      part[(size_t)blockIdx.x * stride + k] = t;
+      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
+    }
+    __shared__ bool flag;
+    if (consumers_last_cta(counter, &flag)) {
+      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+        if (c < k) {
+          sv.c1[c] = s;
+        } else if (c == k) {
+          sv.h->w0 = (double)sqrt_rn(s);
+        } else if (s != T(0)) {
+          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
+          sv.h->done = 1;
+        }
+      });
+    }
+  }
+};
+
 // polynomial preconditioner steps (precond.py:272-319); the SpMV input is
 // `x` of the pipeline; other operands are own-row elementwise.
 template <typename T>
@@ -247,6 +353,25 @@ cudaError_t launch_residual(const CsrView<T>& A, const T* b, const T* x, T* r, d
 template <typename T>
 cudaError_t launch_spmv_dot1(const CsrView<T>& A, const T* x, T* w, const T* V, long long ldv,
                              int k, StateView<T> sv, WsView ws, cudaStream_t st) {
+  auto reg = [&](auto tag) {
+    constexpr int KT = decltype(tag)::value;
+    EpiDot1Reg<T, KT> e{};
+    e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
+    e.part = static_cast<T*>(ws.part);
+    e.counter = ws.counter;
+    return launch_pipeline(A, x, e, (size_t)kSpConsumerWarps * KT * sizeof(T), ws, st);
+  };
+  if (k <= 2) return reg(std::integral_constant<int, 2>{});
+  if (k <= 4) return reg(std::integral_constant<int, 4>{});
+  if (k <= 8) return reg(std::integral_constant<int, 8>{});
+  if (k <= 12) return reg(std::integral_constant<int, 12>{});
+  if (k <= 16) return reg(std::integral_constant<int, 16>{});
+  if (k <= 24) return reg(std::integral_constant<int, 24>{});
+  if (k <= 32) return reg(std::integral_constant<int, 32>{});
+  if (k <= 40) return reg(std::integral_constant<int, 40>{});
+  if (k <= 48) return reg(std::integral_constant<int, 48>{});
+  if (k <= 56) return reg(std::integral_constant<int, 56>{});
+  if (k <= 64) return reg(std::integral_constant<int, 64>{});
   EpiDot1<T> e{};
   e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
   e.part = static_cast<T*>(ws.part);
