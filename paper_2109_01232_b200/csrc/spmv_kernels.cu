@@ -187,6 +187,7 @@ struct EpiDot1Reg {
   // back-to-back 8/16-byte loads (k independent loads in flight per thread).
   __device__ void on_tile(long long a, int nr, const T* ys) {
     const int rr = 2 * (int)threadIdx.x;
+    if (kSpTile < 2 * kSpConsumers && rr >= kSpTile) return;
     if (rr + 1 < nr) {
       const T y0 = ys[rr], y1 = ys[rr + 1];
       const T* v = V + a + rr;
