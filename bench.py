@@ -99,9 +99,13 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # algorithmic byte model
 
-def cycle_bytes(n: int, nnz: int, m: int, s: int) -> dict[str, float]:
-    """Algorithmic bytes per cycle for each fused kernel class, s = value size."""
-    spmv = nnz * (s + 4) + 4 * (n + 1) + 2 * n * s           # CSR + x once + y once
+def cycle_bytes(n: int, nnz: int, m: int, s: int, storage: str = "csr") -> dict[str, float]:
+    """Algorithmic bytes per cycle for each fused kernel class, s = value size.
+    CSR: values + col_idx + row_ptr; stencil: the present values only."""
+    if storage == "stencil":
+        spmv = nnz * s + 2 * n * s                            # values + x once + y once
+    else:
+        spmv = nnz * (s + 4) + 4 * (n + 1) + 2 * n * s       # CSR + x once + y once
     ks = range(1, m + 1)
     return {
         "spmv_dot1": sum(spmv + k * n * s for k in ks),       # + read V[0..k) for pass-1 dots
@@ -167,26 +171,33 @@ def native_arm(args, rank: int, world: int):
     fp64_s = rep64.total_time
     sol_diff = float(torch.linalg.norm(rep64.x - x_ir) / torch.linalg.norm(rep64.x))
 
-    # one profiled (eager) IR cycle: per-kernel-class device time
+    # one profiled (eager) IR cycle per storage: per-kernel-class device time
     A32 = convert_matrix(A, FP32)
     bd = padded_copy(b, FP64)
-    xd = dvec(n, FP64)
-    ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, bd, xd, M, RTOL)
-    ns.begin()
-    ns.cycle(M)                                   # warm
-    prof = ns.profile_cycle(M)
-    ns.close()
-    model = cycle_bytes(n, nnz, M, 4)
-    kernels = {}
-    for k, (ms, cnt) in prof.items():
-        kernels[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}
-        if k in model and ms > 0:
-            kernels[k]["GBps"] = round(model[k] / (ms / 1e3) / 1e9, 1)
+    profiles = {}
+    for storage in ("stencil", "csr"):
+        ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, bd, dvec(n, FP64), M, RTOL, storage=storage)
+        ns.begin()
+        ns.cycle(M)                                   # warm
+        prof = ns.profile_cycle(M)
+        used = ns.storage
+        ns.close()
+        model = cycle_bytes(n, nnz, M, 4, used)
+        kernels = {}
+        for k, (ms, cnt) in prof.items():
+            kernels[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}
+            if k in model and ms > 0:
+                kernels[k]["GBps"] = round(model[k] / (ms / 1e3) / 1e9, 1)
+        cyc_ms = sum(v[0] for v in prof.values())
+        profiles[storage] = {"storage": used, "ms": round(cyc_ms, 4),
+                             "GBps_algorithmic": round(sum(model.values()) / (cyc_ms / 1e3) / 1e9, 1),
+                             "kernels": kernels, "_prof": prof, "_model": model}
     peak, peak_kind = _peaks()
+    main = profiles["stencil"]
+    prof, model = main.pop("_prof"), main.pop("_model")
+    profiles["csr"].pop("_prof"), profiles["csr"].pop("_model")
     dom = max((k for k in model if k in prof), key=lambda k: prof[k][0])
     dom_gbs = model[dom] / (prof[dom][0] / 1e3) / 1e9
-    cyc_ms = sum(v[0] for v in prof.values())
-    cyc_bytes = sum(model.values())
 
     # end to end through the public API with HOST inputs (numpy CSR + b)
     rp, ci, v = A.host_arrays()
@@ -230,8 +241,9 @@ def native_arm(args, rank: int, world: int):
         "speedup_vs_fp64": round(fp64_s / solve_s, 3),
         "solution_rel_diff_ir_vs_fp64": sol_diff,
         "step_times_s": [round(t, 5) for t in times],
-        "profile_cycle": {"ms": round(cyc_ms, 4), "GBps_algorithmic": round(cyc_bytes / (cyc_ms / 1e3) / 1e9, 1),
-                          "kernels": kernels},
+        "storage": main["storage"],
+        "profile_cycle": main,
+        "profile_cycle_csr": profiles["csr"],
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
                      "traffic": None},

@@ -123,6 +123,18 @@ int mpg_generate_stencil(int kind, int64_t nx, double convection, double stretch
                          int64_t row_begin, int64_t row_end, int32_t* row_ptr,
                          int32_t* col_idx, double* values, void* stream);
 
+/* Stencil-specialised SpMV storage (the north star's stencil path).  Checks
+ * that the CSR pattern is exactly the Dirichlet 5-point (dims 2, n = nx^2) or
+ * 7-point (dims 3, n = nx^3) stencil in canonical order and packs the values
+ * slot-major into dia[S][ldv] (S = 5 or 7; absent neighbours stored as 0 and
+ * never read).  *bad (device int32, caller zeroes it) != 0 on mismatch. */
+int mpg_stencil_pack(int prec, int dims, int64_t nx, int64_t n, const int32_t* row_ptr,
+                     const int32_t* col_idx, const void* values, void* dia, int64_t ldv,
+                     int32_t* bad, void* stream);
+/* y = A x from the packed storage; bit-identical to mpg_spmv on the CSR. */
+int mpg_spmv_dia(int prec, int dims, int64_t nx, int64_t n, const void* dia, int64_t ldv,
+                 const void* x, void* y, void* ws, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* Preconditioners (reference precond.py)                                 */
 
@@ -261,6 +273,12 @@ typedef struct {
   void* pc_t2;
   void* pc_t3;
   void* pc_t4;
+  /* stencil-specialised storage (mpg_stencil_pack); stencil_dims 0 = CSR */
+  int32_t stencil_dims;   /* 2: 5-point, 3: 7-point Dirichlet stencil */
+  int32_t stencil_nx;
+  const void* dia;        /* slot-major values, working precision, stride ldv */
+  const double* dia64;    /* IR: fp64 values for the outer residual */
+  const void* pc_dia;     /* poly preconditioner: values in pc_prec */
 } mpg_solver_desc;
 
 typedef struct mpg_solver mpg_solver;

@@ -313,7 +313,52 @@ class CsrMatrix:
                          self.values.clone())
 
     def with_values(self, values: torch.Tensor) -> "CsrMatrix":
-        return CsrMatrix(self.n_rows, self.n_cols, self.row_ptr, self.col_idx, values, _trusted=True)
+        out = CsrMatrix(self.n_rows, self.n_cols, self.row_ptr, self.col_idx, values, _trusted=True)
+        out._stencil = getattr(self, "_stencil", None)   # same pattern, same stencil shape
+        return out
+
+    # --- stencil-specialised storage (mpg_stencil_pack)
+    def stencil_shape(self) -> tuple[int, int] | None:
+        """(dims, nx) if the pattern is exactly a Dirichlet 5-point (2-D) or
+        7-point (3-D) stencil on an nx-grid, else None.  Decided from the
+        sizes, then confirmed on the device by the packing kernel."""
+        cached = getattr(self, "_stencil", None)
+        if cached is not None:
+            return cached or None
+        shape = None
+        n, nnz = self.n_rows, self.nnz
+        if n == self.n_cols and n >= 8:
+            c = round(n ** (1.0 / 3.0))
+            s = round(n ** 0.5)
+            for dims, nx, want in ((3, c, 7 * c ** 3 - 6 * c ** 2), (2, s, 5 * s ** 2 - 4 * s)):
+                if nx >= 2 and nx ** dims == n and nnz == want and n < 2 ** 32:
+                    if self._pack(dims, nx) is not None:
+                        shape = (dims, nx)
+                        break
+        self._stencil = shape if shape else False
+        return shape
+
+    def _pack(self, dims: int, nx: int) -> torch.Tensor | None:
+        S = 7 if dims == 3 else 5
+        ldv = padded_length(self.n_rows)
+        dia = torch.zeros(S * ldv, dtype=self.values.dtype, device=self.values.device)
+        bad = torch.zeros(1, dtype=torch.int32, device=self.values.device)
+        _lib.call("mpg_stencil_pack", self.precision.code, dims, nx, self.n_rows, ptr(self.row_ptr),
+                  ptr(self.col_idx), ptr(self.values), ptr(dia), ldv, ptr(bad), stream_handle())
+        if int(bad.item()) != 0:
+            return None
+        self._dia = dia
+        return dia
+
+    def dia(self) -> torch.Tensor | None:
+        """Slot-major packed values (S x ldv) for the stencil path, or None."""
+        sh = self.stencil_shape()
+        if sh is None:
+            return None
+        d = getattr(self, "_dia", None)
+        if d is None or d.dtype != self.values.dtype:
+            d = self._pack(*sh)
+        return d
 
     def __repr__(self) -> str:
         return f"CsrMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz}, {self.precision.value}, cuda)"

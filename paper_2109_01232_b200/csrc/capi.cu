@@ -124,6 +124,37 @@ int mpg_generate_stencil(int kind, int64_t nx, double conv, double stretch, int6
   return rc(launch_generate(kind, nx, conv, stretch, r0, r1, rp, ci, v, S(stream)));
 }
 
+static int stencil_shape_ok(int dims, int64_t nx, int64_t n) {
+  if ((dims != 2 && dims != 3) || nx < 2) return 0;
+  return n == (dims == 3 ? nx * nx * nx : nx * nx) && n < (1LL << 32);
+}
+
+int mpg_stencil_pack(int prec, int dims, int64_t nx, int64_t n, const int32_t* rp,
+                     const int32_t* ci, const void* v, void* dia, int64_t ldv, int32_t* bad,
+                     void* stream) {
+  if (!stencil_shape_ok(dims, nx, n) || ldv < n || !rp || !dia || !bad) return MPG_EARG;
+  if (prec == MPG_FP64)
+    return rc(launch_stencil_pack<double>(dims, (int)nx, n, rp, ci, (const double*)v, (double*)dia,
+                                          ldv, bad, S(stream)));
+  if (prec == MPG_FP32)
+    return rc(launch_stencil_pack<float>(dims, (int)nx, n, rp, ci, (const float*)v, (float*)dia, ldv,
+                                         bad, S(stream)));
+  return MPG_EARG;
+}
+
+int mpg_spmv_dia(int prec, int dims, int64_t nx, int64_t n, const void* dia, int64_t ldv,
+                 const void* x, void* y, void* ws, void* stream) {
+  if (!stencil_shape_ok(dims, nx, n) || ldv < n || !dia || !ws) return MPG_EARG;
+  WsView w = make_ws(ws);
+  if (prec == MPG_FP64)
+    return rc(launch_spmv<double>(StencilView<double>{(const double*)dia, ldv, n, (int)nx, dims},
+                                  (const double*)x, (double*)y, w, S(stream)));
+  if (prec == MPG_FP32)
+    return rc(launch_spmv<float>(StencilView<float>{(const float*)dia, ldv, n, (int)nx, dims},
+                                 (const float*)x, (float*)y, w, S(stream)));
+  return MPG_EARG;
+}
+
 // ------------------------------------------------------------ preconditioners
 int mpg_jacobi_apply(int prec, int64_t n, int32_t k, const void* lu, const int64_t* piv,
                      const void* x, void* y, void* stream) {

@@ -56,12 +56,44 @@ static mpg_state_header* hdr_of(const mpg_solver_desc& d) {
   return static_cast<mpg_state_header*>(d.state);
 }
 
+template <typename TP, typename F>
+static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, const void* dia,
+                               F&& f);
+
+// r = b - A x, rnorm -> header, in the outer precision (solvers.py:186-188,
+// :205, :330, :358): fp64 for GMRES-IR and fp64 GMRES, fp32 for the fp32 solver.
+static cudaError_t outer_residual(const mpg_solver_desc& d, WsView ws, cudaStream_t st) {
+  mpg_state_header* h = hdr_of(d);
+  if (d.mode == MPG_MODE_IR || d.prec == MPG_FP64) {
+    const double* vals = d.mode == MPG_MODE_IR ? d.values64 : static_cast<const double*>(d.values);
+    const void* dia = d.mode == MPG_MODE_IR ? static_cast<const void*>(d.dia64) : d.dia;
+    return with_matrix<double>(d, vals, dia, [&](const auto& A) {
+      return launch_residual<double>(A, static_cast<const double*>(d.b),
+                                     static_cast<const double*>(d.x), static_cast<double*>(d.r),
+                                     nullptr, h, ws, st);
+    });
+  }
+  return with_matrix<float>(d, static_cast<const float*>(d.values), d.dia, [&](const auto& A) {
+    return launch_residual<float>(A, static_cast<const float*>(d.b), static_cast<const float*>(d.x),
+                                  static_cast<float*>(d.r), nullptr, h, ws, st);
+  });
+}
+
+// Call f with the matrix view the solver uses: the stencil (DIA) storage
+// when the descriptor carries one, the CSR arrays otherwise.
+template <typename TP, typename F>
+static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, const void* dia,
+                               F&& f) {
+  if (d.stencil_dims && dia)
+    return f(StencilView<TP>{static_cast<const TP*>(dia), d.ldv, d.n, d.stencil_nx, d.stencil_dims});
+  return f(CsrView<TP>{d.row_ptr, d.col_idx, csr_vals, d.n});
+}
+
 // Run a lowered polynomial program on x -> y with scratch t0..t2, in TP.
 template <typename TP>
 static cudaError_t run_poly(const mpg_solver_desc& d, const std::vector<mpg_poly_op>& ops,
                             const TP* vals, const TP* x, TP* y, TP* t0, TP* t1, TP* t2,
                             const mpg_state_header* gate, WsView ws, cudaStream_t st) {
-  CsrView<TP> A{d.row_ptr, d.col_idx, vals, d.n};
   TP* bufs[5] = {const_cast<TP*>(x), y, t0, t1, t2};
   for (const mpg_poly_op& op : ops) {
     switch (op.op) {
@@ -71,7 +103,9 @@ static cudaError_t run_poly(const mpg_solver_desc& d, const std::vector<mpg_poly
         TRY(launch_poly_elem<TP>(op.op, (TP)op.a, bufs[op.src], bufs[op.dst], y, d.n, gate, st));
         break;
       default:
-        TRY(launch_poly_op<TP>(A, op, x, y, t0, t1, t2, gate, d.n, ws, st));
+        TRY(with_matrix<TP>(d, vals, d.pc_dia, [&](const auto& A) {
+          return launch_poly_op<TP>(A, op, x, y, t0, t1, t2, gate, d.n, ws, st);
+        }));
     }
   }
   return cudaSuccess;
@@ -171,7 +205,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   WsView ws = make_ws(d.ws);
   T* V = static_cast<T*>(d.V);
   T* w = static_cast<T*>(d.w);
-  CsrView<T> A{d.row_ptr, d.col_idx, static_cast<const T*>(d.values), d.n};
+  const T* vals = static_cast<const T*>(d.values);
   mpg_state_header* h = hdr_of(d);
   // cycle start: gamma, V[:,0] = r0 / gamma
   {
@@ -194,7 +228,12 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
     const T* vj = V + (size_t)j * d.ldv;
     const T* z = nullptr;
     { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
-    { ProfScope ps(PK_SPMV_DOT); TRY(launch_spmv_dot1<T>(A, z, w, V, d.ldv, j + 1, sv, ws, st)); }
+    {
+      ProfScope ps(PK_SPMV_DOT);
+      TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
+        return launch_spmv_dot1<T>(A, z, w, V, d.ldv, j + 1, sv, ws, st);
+      }));
+    }
     { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, w, sv, ws, st)); }
     { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, w, sv, ws, m_limit, st)); }
     { ProfScope ps(PK_SCALE); TRY(launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st)); }
@@ -202,13 +241,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   { ProfScope ps(PK_FINISH); TRY(finish_cycle<T>(s, sv, ws, st)); }
   ProfScope ps(PK_RESIDUAL);
   // explicit residual in the outer precision (solvers.py:205 / :358)
-  if (d.mode == MPG_MODE_IR) {
-    CsrView<double> A64{d.row_ptr, d.col_idx, d.values64, d.n};
-    return launch_residual<double>(A64, static_cast<const double*>(d.b), static_cast<const double*>(d.x),
-                                   static_cast<double*>(d.r), nullptr, h, ws, st);
-  }
-  return launch_residual<T>(A, static_cast<const T*>(d.b), static_cast<const T*>(d.x),
-                            static_cast<T*>(d.r), nullptr, h, ws, st);
+  return outer_residual(d, ws, st);
 }
 
 static cudaError_t enqueue_any(const mpg_solver& s, int m_limit, cudaStream_t st) {
@@ -228,6 +261,13 @@ extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) 
   if (d.mode == MPG_MODE_IR && (d.prec != MPG_FP32 || !d.values64 || !d.r_in)) return MPG_EARG;
   if (!d.row_ptr || !d.col_idx || !d.values || !d.x || !d.b || !d.r || !d.V || !d.w || !d.state || !d.ws)
     return MPG_EARG;
+  if (d.stencil_dims) {
+    if ((d.stencil_dims != 2 && d.stencil_dims != 3) || d.stencil_nx < 2 || !d.dia) return MPG_EARG;
+    const long long nx = d.stencil_nx;
+    if (d.n != (d.stencil_dims == 3 ? nx * nx * nx : nx * nx) || d.n >= (1LL << 32)) return MPG_EARG;
+    if (d.mode == MPG_MODE_IR && !d.dia64) return MPG_EARG;
+    if (d.pc_kind == MPG_PC_POLY && !d.pc_dia) return MPG_EARG;
+  }
   if (d.pc_kind != MPG_PC_NONE) {
     if (d.pc_prec != d.prec && !(d.pc_prec == MPG_FP32 && d.prec == MPG_FP64)) return MPG_EUNSUPPORTED;
     if (d.pc_kind == MPG_PC_JACOBI && (!d.pc_lu || d.pc_block < 1 || d.pc_block > 32)) return MPG_EARG;
@@ -262,22 +302,11 @@ extern "C" int mpg_solver_begin(mpg_solver* s, void* stream) {
   WsView ws = make_ws(d.ws);
   mpg_state_header* h = hdr_of(d);
   const bool outer64 = d.mode == MPG_MODE_IR || d.prec == MPG_FP64;
-  cudaError_t e;
-  if (outer64) {
-    e = launch_norm2<double>(static_cast<const double*>(d.b), d.n, &h->outer_b_norm, ws, st);
-    if (e) return e;
-    const double* vals = d.mode == MPG_MODE_IR ? d.values64 : static_cast<const double*>(d.values);
-    CsrView<double> A{d.row_ptr, d.col_idx, vals, d.n};
-    e = launch_residual<double>(A, static_cast<const double*>(d.b), static_cast<const double*>(d.x),
-                                static_cast<double*>(d.r), nullptr, h, ws, st);
-  } else {
-    e = launch_norm2<float>(static_cast<const float*>(d.b), d.n, &h->outer_b_norm, ws, st);
-    if (e) return e;
-    CsrView<float> A{d.row_ptr, d.col_idx, static_cast<const float*>(d.values), d.n};
-    e = launch_residual<float>(A, static_cast<const float*>(d.b), static_cast<const float*>(d.x),
-                               static_cast<float*>(d.r), nullptr, h, ws, st);
-  }
-  return (int)e;
+  cudaError_t e = outer64
+      ? launch_norm2<double>(static_cast<const double*>(d.b), d.n, &h->outer_b_norm, ws, st)
+      : launch_norm2<float>(static_cast<const float*>(d.b), d.n, &h->outer_b_norm, ws, st);
+  if (e) return e;
+  return (int)outer_residual(d, ws, st);
 }
 
 extern "C" int mpg_solver_cycle(mpg_solver* s, int32_t m_limit, void* stream) {

@@ -37,17 +37,23 @@ struct CsrView {
   long long n;
 };
 
+// shared memory the epilogues use (tile of SpMV results + reduction scratch)
+template <typename T>
+struct alignas(16) EpiShared {
+  alignas(16) T ys[2][kSpTile];
+  T red[32];
+  T acc[8];
+};
+
 template <typename T>
 struct alignas(128) SpSmem {
   alignas(16) int32_t rp[kSpStages][kSpTile + 8];
   alignas(16) int32_t ci[kSpStages][kSpCap];
   alignas(16) T v[kSpStages][kSpCap];
-  alignas(16) T ys[2][kSpTile];
   uint64_t full[kSpStages];
   uint64_t empty[kSpStages];
   int32_t meta[kSpStages][4];  // base, off_ci, off_v, staged
-  T red[32];
-  T acc[8];
+  EpiShared<T> es;
 };
 
 __device__ __forceinline__ void consumer_sync() {
@@ -119,6 +125,81 @@ __device__ __forceinline__ void tile_dots(int k, int nr, const VRow& vrow, const
       acc[threadIdx.x] += s;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Stencil-specialised storage (the north star's "specialised stencil path").
+// For a Dirichlet 5-point (dims 2) or 7-point (dims 3) stencil matrix the
+// pattern is implied by the grid, so only the values are stored, slot-major:
+// slot s of row r at vals[s * ldv + r], slots in ascending column order
+// (3D: z-1, y-1, x-1, c, x+1, y+1, z+1; 2D: y-1, x-1, c, x+1, y+1).  A slot
+// whose neighbour is outside the grid is absent and skipped (never added as
+// a zero), so each row is reduced over exactly the CSR row's entries, in the
+// same order: bit-identical to the CSR kernel and to the reference.
+// Traffic per row drops from nnz_row*(s+4)+4 bytes to S*s bytes of values.
+template <typename T>
+struct StencilView {
+  const T* vals;
+  long long ldv;
+  long long n;
+  int nx;
+  int dims;
+};
+
+template <typename T>
+__device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __restrict__ x,
+                                         long long r) {
+  const unsigned nx = (unsigned)S.nx;
+  const unsigned ur = (unsigned)r;
+  const unsigned ix = ur % nx;
+  const unsigned q = ur / nx;
+  bool have = false;
+  T p0 = T(0), rest = T(-0.0);
+  const T* v = S.vals + r;
+  auto term = [&](bool present, int slot, long long off) {
+    if (present) {
+      const T p = mul_rn(__ldg(v + (size_t)slot * S.ldv), __ldg(x + r + off));
+      if (!have) { p0 = p; have = true; }
+      else rest = add_rn(rest, p);
+    }
+  };
+  if (S.dims == 3) {
+    const unsigned iy = q % nx, iz = q / nx;
+    const long long p2 = (long long)nx * nx;
+    term(iz > 0, 0, -p2);
+    term(iy > 0, 1, -(long long)nx);
+    term(ix > 0, 2, -1);
+    term(true, 3, 0);
+    term(ix + 1 < nx, 4, 1);
+    term(iy + 1 < nx, 5, (long long)nx);
+    term(iz + 1 < nx, 6, p2);
+  } else {
+    const unsigned iy = q;
+    term(iy > 0, 0, -(long long)nx);
+    term(ix > 0, 1, -1);
+    term(true, 2, 0);
+    term(ix + 1 < nx, 3, 1);
+    term(iy + 1 < nx, 4, (long long)nx);
+  }
+  // add.reduceat order for rows of <= 8 entries: p0 + (((p1 + p2) + p3) ...)
+  return add_rn(p0, rest);
+}
+
+template <typename T, typename E>
+__device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
+                                                 E& epi, EpiShared<T>& es) {
+  long long R0, R1;
+  cta_rows(S.n, R0, R1);
+  int t = 0;
+  for (long long a = R0; a < R1; a += kSpTile, ++t) {
+    const int nrows = (int)min((long long)kSpTile, R1 - a);
+    T* ys = es.ys[t & 1];
+    for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
+      ys[rr] = epi.on_row(a + rr, stencil_row(S, x, a + rr));
+    consumer_sync();
+    epi.on_tile(a, nrows, ys);
+  }
+  epi.on_end();
 }
 
 template <typename T, typename E>
@@ -195,7 +276,7 @@ __device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __re
     const int base = sm.meta[s][0];
     const bool staged = sm.meta[s][3] != 0;
     const int32_t* rps = sm.rp[s];
-    T* ys = sm.ys[t & 1];
+    T* ys = sm.es.ys[t & 1];
     for (int rr = tid; rr < nrows; rr += kSpConsumers) {
       const int lo = rps[rr], hi = rps[rr + 1];
       T y;

@@ -45,7 +45,7 @@ template <typename T>
 struct EpiPlain {
   T* y;
   __device__ bool skip() const { return false; }
-  __device__ void init(SpSmem<T>&, unsigned char*) {}
+  __device__ void init(EpiShared<T>&, unsigned char*) {}
   __device__ T on_row(long long r, T v) { y[r] = v; return v; }
   __device__ void on_tile(long long, int, const T*) {}
   __device__ void on_end() {}
@@ -61,9 +61,9 @@ struct EpiResid {
   T* part;
   unsigned int* counter;
   T ss;
-  SpSmem<T>* sm;
+  EpiShared<T>* sm;
   __device__ bool skip() const { return false; }
-  __device__ void init(SpSmem<T>& s, unsigned char*) { sm = &s; ss = T(0); }
+  __device__ void init(EpiShared<T>& s, unsigned char*) { sm = &s; ss = T(0); }
   __device__ T on_row(long long i, T y) {
     const T v = sub_rn(__ldg(b + i), y);
     r[i] = v;
@@ -98,9 +98,9 @@ struct EpiDot1 {
   T ss;
   int bad;
   T* acc;
-  SpSmem<T>* sm;
+  EpiShared<T>* sm;
   __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
-  __device__ void init(SpSmem<T>& s, unsigned char* extra) {
+  __device__ void init(EpiShared<T>& s, unsigned char* extra) {
     sm = &s;
     acc = reinterpret_cast<T*>(extra);
     for (int i = threadIdx.x; i < k; i += blockDim.x) acc[i] = T(0);
@@ -166,9 +166,9 @@ struct EpiDot1Reg {
   int bad;
   T acc[KT];
   T* red2;   // [kSpConsumerWarps][KT] in dynamic smem
-  SpSmem<T>* sm;
+  EpiShared<T>* sm;
   __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
-  __device__ void init(SpSmem<T>& s, unsigned char* extra) {
+  __device__ void init(EpiShared<T>& s, unsigned char* extra) {
     sm = &s;
     red2 = reinterpret_cast<T*>(extra);
 #pragma unroll
@@ -267,7 +267,7 @@ struct EpiPoly {
   T* y;           // accumulator (NEWTON_REAL, PAIR1)
   const mpg_state_header* gate;
   __device__ bool skip() const { return gate && *(volatile const int*)&gate->done != 0; }
-  __device__ void init(SpSmem<T>&, unsigned char*) {}
+  __device__ void init(EpiShared<T>&, unsigned char*) {}
   __device__ T on_row(long long i, T v) {
     switch (op) {
       case MPG_POLY_HORNER: {  // y = spmv(A, y); y += c[i] * x
@@ -307,15 +307,75 @@ __global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __re
   extern __shared__ __align__(128) unsigned char smraw[];
   if (epi.skip()) return;
   SpSmem<T>& sm = *reinterpret_cast<SpSmem<T>*>(smraw);
-  epi.init(sm, smraw + sizeof(SpSmem<T>));
+  epi.init(sm.es, smraw + sizeof(SpSmem<T>));
   spmv_pipeline(A, x, epi, sm);
+}
+
+template <typename T, typename E>
+__global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, const T* __restrict__ x,
+                                                          E epi) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ EpiShared<T> es;
+  if (epi.skip()) return;
+  epi.init(es, smraw);
+  stencil_pipeline(S, x, epi, es);
+}
+
+// DIA packing + pattern check: one thread per row.  *bad != 0 when the CSR
+// pattern is not exactly the Dirichlet 5/7-point stencil of the grid.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, long long n,
+                                                           const int32_t* __restrict__ rp,
+                                                           const int32_t* __restrict__ ci,
+                                                           const T* __restrict__ v, T* out,
+                                                           long long ldv, int* bad) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const unsigned unx = (unsigned)nx, ur = (unsigned)r;
+    const unsigned ix = ur % unx, q = ur / unx;
+    bool pres[7];
+    long long off[7];
+    int S;
+    if (dims == 3) {
+      const unsigned iy = q % unx, iz = q / unx;
+      const long long p2 = (long long)nx * nx;
+      S = 7;
+      pres[0] = iz > 0; off[0] = -p2;
+      pres[1] = iy > 0; off[1] = -(long long)nx;
+      pres[2] = ix > 0; off[2] = -1;
+      pres[3] = true; off[3] = 0;
+      pres[4] = ix + 1 < unx; off[4] = 1;
+      pres[5] = iy + 1 < unx; off[5] = nx;
+      pres[6] = iz + 1 < unx; off[6] = p2;
+    } else {
+      S = 5;
+      pres[0] = q > 0; off[0] = -(long long)nx;
+      pres[1] = ix > 0; off[1] = -1;
+      pres[2] = true; off[2] = 0;
+      pres[3] = ix + 1 < unx; off[3] = 1;
+      pres[4] = q + 1 < unx; off[4] = nx;
+    }
+    int p = rp[r];
+    const int e = rp[r + 1];
+    int ok = 1;
+    for (int sl = 0; sl < S; ++sl) {
+      T val = T(0);
+      if (pres[sl]) {
+        if (p < e && (long long)ci[p] == r + off[sl]) val = v[p++];
+        else ok = 0;
+      }
+      out[(size_t)sl * ldv + r] = val;
+    }
+    if (p != e) ok = 0;
+    if (!ok) atomicOr(bad, 1);
+  }
 }
 
 // ----------------------------------------------------------------- launches
 
 template <typename T, typename E>
-static cudaError_t launch_pipeline(const CsrView<T>& A, const T* x, const E& epi, size_t extra,
-                                   WsView, cudaStream_t st) {
+static cudaError_t launch_matrix(const CsrView<T>& A, const T* x, const E& epi, size_t extra,
+                                 cudaStream_t st) {
   const size_t smem = sizeof(SpSmem<T>) + extra;
   static std::once_flag once;
   static int occ = 1;
@@ -335,32 +395,54 @@ static cudaError_t launch_pipeline(const CsrView<T>& A, const T* x, const E& epi
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_spmv(const CsrView<T>& A, const T* x, T* y, WsView ws, cudaStream_t st) {
-  EpiPlain<T> e{y};
-  return launch_pipeline(A, x, e, 0, ws, st);
+template <typename T, typename E>
+static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& epi, size_t extra,
+                                 cudaStream_t st) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [&] {
+    cudaFuncSetAttribute(k_stencil<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)(kMaxM + 8) * sizeof(T) * 8));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<T, E>, kSpConsumers, extra);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  long long tiles = (S.n + kSpTile - 1) / kSpTile;
+  long long G = (long long)num_sms() * occ;
+  if (tiles < G) G = tiles;
+  if (G > kMaxParts) G = kMaxParts;
+  if (G < 1) G = 1;
+  count_launch();
+  k_stencil<T, E><<<(unsigned)G, kSpConsumers, extra, st>>>(S, x, epi);
+  return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_residual(const CsrView<T>& A, const T* b, const T* x, T* r, double* norm_out,
+template <typename T, typename M>
+cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView, cudaStream_t st) {
+  EpiPlain<T> e{y};
+  return launch_matrix(A, x, e, 0, st);
+}
+
+template <typename T, typename M>
+cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
                             mpg_state_header* hdr, WsView ws, cudaStream_t st) {
   EpiResid<T> e{};
   e.b = b; e.r = r; e.out = norm_out; e.hdr = hdr;
   e.part = static_cast<T*>(ws.part);
   e.counter = ws.counter;
-  return launch_pipeline(A, x, e, 0, ws, st);
+  return launch_matrix(A, x, e, 0, st);
 }
 
-template <typename T>
-cudaError_t launch_spmv_dot1(const CsrView<T>& A, const T* x, T* w, const T* V, long long ldv,
-                             int k, StateView<T> sv, WsView ws, cudaStream_t st) {
+template <typename T, typename M>
+cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
+                             StateView<T> sv, WsView ws, cudaStream_t st) {
   auto reg = [&](auto tag) {
     constexpr int KT = decltype(tag)::value;
     EpiDot1Reg<T, KT> e{};
     e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
     e.part = static_cast<T*>(ws.part);
     e.counter = ws.counter;
-    return launch_pipeline(A, x, e, (size_t)kSpConsumerWarps * KT * sizeof(T), ws, st);
+    return launch_matrix(A, x, e, (size_t)kSpConsumerWarps * KT * sizeof(T), st);
   };
   if (k <= 2) return reg(std::integral_constant<int, 2>{});
   if (k <= 4) return reg(std::integral_constant<int, 4>{});
@@ -377,12 +459,12 @@ cudaError_t launch_spmv_dot1(const CsrView<T>& A, const T* x, T* w, const T* V, 
   e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
   e.part = static_cast<T*>(ws.part);
   e.counter = ws.counter;
-  return launch_pipeline(A, x, e, (size_t)(k + 8) * sizeof(T), ws, st);
+  return launch_matrix(A, x, e, (size_t)(k + 8) * sizeof(T), st);
 }
 
-template <typename T>
-cudaError_t launch_poly_op(const CsrView<T>& A, const mpg_poly_op& op, const T* x, T* y, T* t0,
-                           T* t1, T* t2, const mpg_state_header* gate, long long n, WsView ws,
+template <typename T, typename M>
+cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, T* t0, T* t1,
+                           T* t2, const mpg_state_header* gate, long long n, WsView ws,
                            cudaStream_t st) {
   T* bufs[5] = {const_cast<T*>(x), y, t0, t1, t2};
   EpiPoly<T> e{};
@@ -394,20 +476,37 @@ cudaError_t launch_poly_op(const CsrView<T>& A, const mpg_poly_op& op, const T* 
   e.x2 = bufs[op.x2];
   e.y = y;
   e.gate = gate;
-  return launch_pipeline(A, e.src, e, 0, ws, st);
+  return launch_matrix(A, e.src, e, 0, st);
 }
 
-#define INST(T)                                                                                 \
-  template cudaError_t launch_spmv<T>(const CsrView<T>&, const T*, T*, WsView, cudaStream_t);   \
-  template cudaError_t launch_residual<T>(const CsrView<T>&, const T*, const T*, T*, double*,   \
-                                          mpg_state_header*, WsView, cudaStream_t);            \
-  template cudaError_t launch_spmv_dot1<T>(const CsrView<T>&, const T*, T*, const T*, long long, \
-                                           int, StateView<T>, WsView, cudaStream_t);          \
-  template cudaError_t launch_poly_op<T>(const CsrView<T>&, const mpg_poly_op&, const T*, T*,  \
-                                         T*, T*, T*, const mpg_state_header*, long long,       \
-                                         WsView, cudaStream_t);
-INST(float)
-INST(double)
-#undef INST
+template <typename T>
+cudaError_t launch_stencil_pack(int dims, int nx, long long n, const int32_t* rp, const int32_t* ci,
+                                const T* v, T* out, long long ldv, int* bad, cudaStream_t st) {
+  long long G = (n + kThreads - 1) / kThreads;
+  if (G > (long long)num_sms() * 8) G = (long long)num_sms() * 8;
+  if (G < 1) G = 1;
+  count_launch();
+  k_stencil_pack<T><<<(unsigned)G, kThreads, 0, st>>>(dims, nx, n, rp, ci, v, out, ldv, bad);
+  return cudaGetLastError();
+}
+
+#define INST_M(T, M)                                                                            \
+  template cudaError_t launch_spmv<T, M>(const M&, const T*, T*, WsView, cudaStream_t);         \
+  template cudaError_t launch_residual<T, M>(const M&, const T*, const T*, T*, double*,         \
+                                             mpg_state_header*, WsView, cudaStream_t);         \
+  template cudaError_t launch_spmv_dot1<T, M>(const M&, const T*, T*, const T*, long long, int, \
+                                              StateView<T>, WsView, cudaStream_t);             \
+  template cudaError_t launch_poly_op<T, M>(const M&, const mpg_poly_op&, const T*, T*, T*, T*, \
+                                            T*, const mpg_state_header*, long long, WsView,    \
+                                            cudaStream_t);
+INST_M(float, CsrView<float>)
+INST_M(double, CsrView<double>)
+INST_M(float, StencilView<float>)
+INST_M(double, StencilView<double>)
+#undef INST_M
+template cudaError_t launch_stencil_pack<float>(int, int, long long, const int32_t*, const int32_t*,
+                                                const float*, float*, long long, int*, cudaStream_t);
+template cudaError_t launch_stencil_pack<double>(int, int, long long, const int32_t*, const int32_t*,
+                                                 const double*, double*, long long, int*, cudaStream_t);
 
 }  // namespace mpg

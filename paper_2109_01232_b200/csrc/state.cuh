@@ -82,22 +82,26 @@ inline WsView make_ws(void* base) {
 // ------------------------------------------------------------- launchers
 void count_launch(int n = 1);
 
-// CSR views (defined in spmv.cuh)
+// matrix views (defined in spmv.cuh): CSR and the stencil (DIA) storage
 template <typename T> struct CsrView;
+template <typename T> struct StencilView;
 
-// spmv family (spmv_kernels.cu)
-template <typename T>
-cudaError_t launch_spmv(const CsrView<T>& A, const T* x, T* y, WsView ws, cudaStream_t st);
-template <typename T>
-cudaError_t launch_residual(const CsrView<T>& A, const T* b, const T* x, T* r, double* norm_out,
+// spmv family (spmv_kernels.cu); M = CsrView<T> or StencilView<T>
+template <typename T, typename M>
+cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView ws, cudaStream_t st);
+template <typename T, typename M>
+cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
                             mpg_state_header* hdr, WsView ws, cudaStream_t st);
+template <typename T, typename M>
+cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
+                             StateView<T> sv, WsView ws, cudaStream_t st);
+template <typename T, typename M>
+cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, T* t0, T* t1,
+                           T* t2, const mpg_state_header* gate, long long n, WsView ws,
+                           cudaStream_t st);
 template <typename T>
-cudaError_t launch_spmv_dot1(const CsrView<T>& A, const T* x, T* w, const T* V, long long ldv,
-                             int k, StateView<T> sv, WsView ws, cudaStream_t st);
-template <typename T>
-cudaError_t launch_poly_op(const CsrView<T>& A, const mpg_poly_op& op, const T* x, T* y, T* t0,
-                           T* t1, T* t2, const mpg_state_header* gate, long long n,
-                           WsView ws, cudaStream_t st);
+cudaError_t launch_stencil_pack(int dims, int nx, long long n, const int32_t* rp, const int32_t* ci,
+                                const T* v, T* out, long long ldv, int* bad, cudaStream_t st);
 
 // arnoldi family (arnoldi_kernels.cu)
 template <typename T>

@@ -107,7 +107,15 @@ def generate(spec) -> CsrMatrix:
     """The stencil matrix in fp64 canonical CSR, assembled on the device."""
     n, _ = stencil_counts(spec)
     rp, ci, v = generate_rows(spec, 0, n)
-    return CsrMatrix(n, n, rp, ci, v, _trusted=True)
+    A = CsrMatrix(n, n, rp, ci, v, _trusted=True)
+    kind = spec.kind.value if hasattr(spec.kind, "value") else str(spec.kind)
+    if kind == "laplace3d":
+        A._stencil = (3, int(spec.nx))
+    elif kind in ("laplace2d", "convdiff2d", "recirc2d", "stretched2d"):
+        A._stencil = (2, int(spec.nx))
+    else:
+        A._stencil = False
+    return A
 
 
 def make_rhs(spec: RhsSpec, n: int, *, on_device: bool = False):

@@ -213,7 +213,7 @@ class NativeSolve:
 
     def __init__(self, mode: int, prec: Precision, A: CsrMatrix, A64: CsrMatrix | None,
                  b: torch.Tensor, x: torch.Tensor, m: int, rtol: float,
-                 pc: _Prepared | None = None, use_graph: bool = True):
+                 pc: _Prepared | None = None, use_graph: bool = True, storage: str = "auto"):
         self.mode, self.prec, self.m, self.n = mode, prec, m, A.n_rows
         n = self.n
         outer = FP64 if mode == _lib.MODE_IR else prec
@@ -253,6 +253,30 @@ class NativeSolve:
                 d.pc_ops, d.pc_nops = ops, len(pc.ops)
                 d.pc_values = ptr(pc.values)
                 self._keep.append(pc.values)
+        # stencil-specialised storage: every SpMV of the cycle (Arnoldi operator,
+        # polynomial steps, explicit residual) reads packed values instead of CSR
+        self.storage = "csr"
+        if storage not in ("auto", "csr", "stencil"):
+            raise ValueError("storage must be 'auto', 'csr' or 'stencil'")
+        if storage != "csr":
+            shape = A.stencil_shape()
+            if shape is None and storage == "stencil":
+                raise ValueError("the matrix is not a 5/7-point Dirichlet stencil")
+            if shape is not None:
+                dia = A.dia()
+                dia64 = A64.dia() if A64 is not None else None
+                pc_dia = None
+                if pc is not None and pc.kind == _lib.PC_POLY:
+                    pcm = A.with_values(pc.values)
+                    pc_dia = pcm.dia()
+                if dia is not None and (A64 is None or dia64 is not None) and \
+                        (pc is None or pc.kind != _lib.PC_POLY or pc_dia is not None):
+                    d.stencil_dims, d.stencil_nx = shape
+                    d.dia = ptr(dia)
+                    d.dia64 = ptr(dia64) if dia64 is not None else None
+                    d.pc_dia = ptr(pc_dia) if pc_dia is not None else None
+                    self._keep += [t for t in (dia, dia64, pc_dia) if t is not None]
+                    self.storage = "stencil"
         self.desc = d
         h = C.c_void_p()
         _lib.call("mpg_solver_create", C.byref(d), C.byref(h))
@@ -366,7 +390,7 @@ def _as_vector(v, prec: Precision) -> torch.Tensor:
 def gmres_restarted(A, b, x0=None, criteria: StopCriteria | None = None, precond=None,
                     precision: Precision | None = None, *,
                     timer: timing.KernelTimer | None = None, stop_on_stall: bool = False,
-                    use_graph: bool = True) -> SolveReport:
+                    use_graph: bool = True, storage: str = "auto") -> SolveReport:
     """Restarted GMRES in one working precision (solvers.py:251-294)."""
     criteria = criteria or StopCriteria()
     host = not isinstance(b, torch.Tensor)
@@ -384,7 +408,7 @@ def gmres_restarted(A, b, x0=None, criteria: StopCriteria | None = None, precond
     history: list[HistoryEntry] = []
     phase = _phase_of(precision)
     ns = NativeSolve(_lib.MODE_RESTARTED, precision, A, None, bd, xd, criteria.m, criteria.rtol,
-                     pc, use_graph)
+                     pc, use_graph, storage)
     try:
         with timing.active(timer):
             converged, total, loss, stalled_at = _run_restarted(
@@ -403,7 +427,7 @@ def gmres_restarted(A, b, x0=None, criteria: StopCriteria | None = None, precond
 
 
 def gmres_ir(A, b, x0=None, criteria: StopCriteria | None = None, precond_fp32=None, *,
-             timer: timing.KernelTimer | None = None, use_graph: bool = True) -> SolveReport:
+             timer: timing.KernelTimer | None = None, use_graph: bool = True, storage: str = "auto") -> SolveReport:
     """GMRES-IR: fp32 correction cycles, fp64 residual updates (solvers.py:297-384).
 
     The fp32 copy of A is made up front and excluded from ``total_time``, as in
@@ -427,7 +451,8 @@ def gmres_ir(A, b, x0=None, criteria: StopCriteria | None = None, precond_fp32=N
     pc = _prepare_precond(precond_fp32, A32, FP32)
     timer = timer if timer is not None else timing.KernelTimer()
     history: list[HistoryEntry] = []
-    ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, bd, xd, criteria.m, criteria.rtol, pc, use_graph)
+    ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, bd, xd, criteria.m, criteria.rtol, pc, use_graph,
+                     storage)
     try:
         with timing.active(timer):
             b_norm, rnorm = ns.begin()                      # suspended in the reference (:328-330)
@@ -469,7 +494,7 @@ def gmres_ir(A, b, x0=None, criteria: StopCriteria | None = None, precond_fp32=N
 
 
 def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: int = 0, *,
-             timer: timing.KernelTimer | None = None, use_graph: bool = True) -> SolveReport:
+             timer: timing.KernelTimer | None = None, use_graph: bool = True, storage: str = "auto") -> SolveReport:
     """fp32 leg up to ``switch_iter`` (or a stall), then fp64 (solvers.py:387-440)."""
     criteria = criteria or StopCriteria()
     if switch_iter < 0 or switch_iter % criteria.m != 0:
@@ -492,7 +517,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
         b32 = _as_vector(bd[:n], FP32)
         x32 = _as_vector(xd[:n], FP32)
         ns32 = NativeSolve(_lib.MODE_RESTARTED, FP32, A32, None, b32, x32, criteria.m,
-                           criteria.rtol, None, use_graph)
+                           criteria.rtol, None, use_graph, storage)
         try:
             with timing.active(timer):
                 _, iters32, loss32, stalled_at = _run_restarted(
@@ -504,7 +529,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
         if history and history[-1].iteration == iters32:
             history.pop()
     ns = NativeSolve(_lib.MODE_RESTARTED, FP64, A, None, bd, xd, criteria.m, criteria.rtol,
-                     None, use_graph)
+                     None, use_graph, storage)
     try:
         with timing.active(timer):
             converged, iters64, loss64, st64 = _run_restarted(

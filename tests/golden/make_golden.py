@@ -51,6 +51,9 @@ def report_dict(rep) -> dict:
         "x_sha256": sha(rep.x),
         "x_norm": float(np.linalg.norm(rep.x)),
         "x_head": [float(v) for v in rep.x[:4]],
+        # strided sample of the solution (full x is too large to commit at cfg2)
+        "x_stride": max(1, len(rep.x) // 4096),
+        "x_sample": [float(v) for v in rep.x[:: max(1, len(rep.x) // 4096)]],
         "total_time_s": float(rep.total_time),
     }
 

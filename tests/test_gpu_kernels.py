@@ -190,3 +190,42 @@ def test_poly_build_on_device_close_to_oracle():
         # same polynomial up to the (different) reduction order of the build's dots
         y, yo = P.apply_poly(M, A, x), O.poly_apply(Mo, Ao, x)
         assert np.linalg.norm(y - yo) <= 1e-7 * np.linalg.norm(yo)
+
+
+@pytest.mark.parametrize("kind,nx,kw", [("laplace3d", 23, {}), ("laplace2d", 37, {}),
+                                        ("convdiff2d", 41, {"convection": 1501.0}),
+                                        ("recirc2d", 33, {"convection": 40.1}),
+                                        ("stretched2d", 17, {}), ("laplace3d", 2, {})])
+def test_stencil_storage_bitexact(kind, nx, kw, rng):
+    """The stencil-specialised SpMV (packed values, no col_idx) equals the CSR
+    kernel and the oracle bit for bit, in both precisions."""
+    import ctypes as C
+    from paper_2109_01232_b200.core import ctx, padded_length, stream_handle
+    Ao = O.stencil_csr(kind, nx, **kw)
+    A = P.CsrMatrix(Ao.n_rows, Ao.n_cols, Ao.row_ptr, Ao.col_idx, Ao.values)   # uploaded, not tagged
+    dims, nxd = A.stencil_shape()
+    assert (dims, nxd) == ((3 if kind == "laplace3d" else 2), nx)
+    for dt in (np.float64, np.float32):
+        Ad = A if dt == np.float64 else P.convert_matrix(A, P.FP32)
+        dia = Ad.dia()
+        x = rng.standard_normal(Ao.n_cols).astype(dt)
+        xd = torch.from_numpy(x).cuda()
+        y = torch.empty_like(xd)
+        _lib.call("mpg_spmv_dia", Ad.precision.code, dims, nx, Ao.n_rows, dia.data_ptr(),
+                  padded_length(Ao.n_rows), xd.data_ptr(), y.data_ptr(), ctx().ws.data_ptr(),
+                  stream_handle())
+        assert bits_equal(y.cpu().numpy(), O.spmv(Ao.astype(dt), x)), (kind, dt)
+
+
+def test_stencil_detection_rejects_non_stencils():
+    d = np.diag(np.full(64, 2.0)) + np.diag(np.full(63, -1.0), 1)
+    assert P.CsrMatrix.from_dense(d).stencil_shape() is None
+    Ao = O.stencil_csr("star2d", 8)
+    assert P.CsrMatrix(Ao.n_rows, Ao.n_cols, Ao.row_ptr, Ao.col_idx, Ao.values).stencil_shape() is None
+    # same sizes as a 5-point stencil but one entry moved: the device check rejects it
+    Ao = O.stencil_csr("laplace2d", 8)
+    ci = Ao.col_idx.copy()
+    ci[10] = ci[10] + 1 if ci[10] + 1 < ci[11] else ci[10]
+    A = P.CsrMatrix(Ao.n_rows, Ao.n_cols, Ao.row_ptr, np.where(np.arange(len(ci)) == 3, ci[3] + 1, ci),
+                    Ao.values)
+    assert A.stencil_shape() is None

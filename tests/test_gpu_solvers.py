@@ -234,3 +234,26 @@ def test_native_code_launched():
     A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE2D, 30))
     P.gmres_ir(A, np.ones(A.n_rows))
     assert _lib.launch_count() - before > 100
+
+
+@pytest.mark.parametrize("solver", ["fp64", "ir", "fd"])
+def test_stencil_storage_solves_bitwise_equal_to_csr(solver):
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, 24))
+    b = np.ones(A.n_rows)
+    kw = {"criteria": P.StopCriteria(m=30)}
+    f = {"fp64": P.gmres_restarted, "ir": P.gmres_ir,
+         "fd": lambda A, b, **k: P.gmres_fd(A, b, switch_iter=60, **k)}[solver]
+    r_csr = f(A, b, storage="csr", **kw)
+    r_st = f(A, b, storage="stencil", **kw)
+    assert r_csr.total_iters == r_st.total_iters
+    assert np.array_equal(r_csr.x, r_st.x)
+    assert r_csr.residual_history == r_st.residual_history
+
+
+def test_stencil_storage_with_preconditioners():
+    Ao = O.stencil_csr("laplace3d", 16)
+    A, b = dev(Ao), np.ones(Ao.n_rows)
+    for M in (O.poly_build(Ao.astype(np.float32), 12, seed=0), O.jacobi_build(Ao.astype(np.float32), 1)):
+        r1 = P.gmres_ir(A, b, precond_fp32=M, storage="csr")
+        r2 = P.gmres_ir(A, b, precond_fp32=M, storage="stencil")
+        assert r1.total_iters == r2.total_iters and np.array_equal(r1.x, r2.x)
