@@ -211,6 +211,219 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_reg(const T* __restrict
   (void)lastflag;
 }
 
+// ========================= K_B, quad-split register variant (k <= KT <= 64)
+// The 4 lanes of a quad share a 2-row segment; lane j owns basis vectors
+// i = 4q + j.  Each lane loads its vectors' 2-row slices once (8/16-byte
+// loads; the quad together reads a contiguous 2-row segment of 4 vectors),
+// forms its part of u = V c1, the quad completes u with two xor-shuffles,
+// every lane applies w' = w - u and accumulates its KT/4 pass-2 dots.  KT/4
+// accumulators per thread (instead of KT) keep occupancy high, so enough
+// loads are in flight to stream V at HBM rate.
+template <typename T, int KT>
+__global__ void __launch_bounds__(kThreads) k_update_dot_q(const T* __restrict__ V, long long ldv,
+                                                           long long n, int k, T* __restrict__ w,
+                                                           StateView<T> sv, WsView ws) {
+  if (gated(sv.h)) return;
+  constexpr int KQ = KT / 4;
+  __shared__ T c1s[KT];
+  __shared__ T red2[kWarps][KT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j = tid & 3, quad = tid >> 2;
+  if (tid < KT) c1s[tid] = tid < k ? sv.c1[tid] : T(0);
+  __syncthreads();
+  T c1q[KQ], acc[KQ];
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    c1q[q] = c1s[4 * q + j];
+    acc[q] = T(0);
+  }
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  // warp-uniform trip count (the quad shuffles below need every lane)
+  for (long long wb = R0 + 16 * warp; wb < R1; wb += 2 * (kThreads / 4)) {
+    const long long rb = wb + 2 * (quad & 7);
+    const bool one = rb < R1;
+    const bool two = rb + 1 < R1;
+    T v0[KQ], v1[KQ];
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int i = 4 * q + j;
+      v0[q] = T(0);
+      v1[q] = T(0);
+      if (i < k && one) {
+        const T* p = V + (size_t)i * ldv + rb;
+        if (two) {
+          if constexpr (sizeof(T) == 4) {
+            const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+            v0[q] = t.x; v1[q] = t.y;
+          } else {
+            const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+            v0[q] = t.x; v1[q] = t.y;
+          }
+        } else {
+          v0[q] = __ldcs(p);
+        }
+      }
+    }
+    T u0 = T(0), u1 = T(0);
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      u0 = fma_rn(v0[q], c1q[q], u0);
+      u1 = fma_rn(v1[q], c1q[q], u1);
+    }
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
+    u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
+    u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
+    const T x0 = one ? sub_rn(w[rb], u0) : T(0);
+    const T x1 = two ? sub_rn(w[rb + 1], u1) : T(0);
+    if (j == 0 && one) {
+      w[rb] = x0;
+      if (two) w[rb + 1] = x1;
+    }
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) acc[q] = fma_rn(v1[q], x1, fma_rn(v0[q], x0, acc[q]));
+  }
+  // lanes with equal j hold the same vectors: reduce across quads (xor 4, 8, 16)
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    T a = acc[q];
+    a += __shfl_xor_sync(0xffffffffu, a, 4);
+    a += __shfl_xor_sync(0xffffffffu, a, 8);
+    a += __shfl_xor_sync(0xffffffffu, a, 16);
+    if (lane < 4) red2[warp][4 * q + lane] = a;
+  }
+  __syncthreads();
+  T* part = static_cast<T*>(ws.part);
+  if (tid < k) {
+    T s = T(0);
+    for (int q = 0; q < kWarps; ++q) s += red2[q][tid];
+    part[(size_t)blockIdx.x * k + tid] = s;
+  }
+  if (last_cta(ws.counter)) {
+    const int jj = k - 1;
+    for (int c = warp; c < k; c += kWarps) {
+      T s2 = T(0);
+      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        sv.c2[c] = s2;
+        sv.Hc(jj, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
+      }
+    }
+  }
+}
+
+// ========================= K_B, warp-owned-vector variant (k <= 8*KV <= 64)
+// Warp w owns basis vectors i = w + 8q (q < KV).  Per block of RB = 32*VN
+// rows each lane loads one 16-byte slice of each owned vector (a warp-wide
+// load = 512 contiguous bytes of one vector), forms its warp's partial
+// u_w = sum_q V_i c1_i, and the 8 partials are summed in a fixed order
+// through a double-buffered shared array (one barrier per block).  Then
+// w' = w - u and the lane's KV pass-2 accumulators.  V is read once; per
+// lane registers hold KV slices and KV accumulators.
+template <typename T, int KV>
+__global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__ V, long long ldv,
+                                                           long long n, int k, T* __restrict__ w,
+                                                           StateView<T> sv, WsView ws) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  constexpr int RB = 32 * VN;
+  __shared__ __align__(16) T upart[2][kWarps][RB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  T c1q[KV], acc[KV];
+#pragma unroll
+  for (int q = 0; q < KV; ++q) {
+    const int i = warp + kWarps * q;
+    c1q[q] = i < k ? sv.c1[i] : T(0);
+    acc[q] = T(0);
+  }
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  int it = 0;
+  for (long long rb = R0; rb < R1; rb += RB, ++it) {
+    const long long r = rb + (long long)lane * VN;
+    const bool full = r + VN <= R1;
+    T v[KV][VN];
+#pragma unroll
+    for (int q = 0; q < KV; ++q) {
+      const int i = warp + kWarps * q;
+      if (i < k && full) {
+        vload_cs(V + (size_t)i * ldv + r, v[q]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) v[q][e] = (i < k && r + e < R1) ? __ldcs(V + (size_t)i * ldv + r + e) : T(0);
+      }
+    }
+    // every warp reads this block of w before the barrier; warp 0 overwrites
+    // it only after the barrier, so no warp can observe the updated values
+    T wv[VN];
+    if (full) {
+      const auto q4 = *reinterpret_cast<const typename Vec<T>::type*>(w + r);
+      if constexpr (VN == 4) { wv[0] = q4.x; wv[1] = q4.y; wv[2] = q4.z; wv[3] = q4.w; }
+      else { wv[0] = q4.x; wv[1] = q4.y; }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VN; ++e) wv[e] = (r + e < R1) ? w[r + e] : T(0);
+    }
+    T u[VN];
+#pragma unroll
+    for (int e = 0; e < VN; ++e) u[e] = T(0);
+#pragma unroll
+    for (int q = 0; q < KV; ++q)
+#pragma unroll
+      for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c1q[q], u[e]);
+    T* up = upart[it & 1][warp] + lane * VN;
+#pragma unroll
+    for (int e = 0; e < VN; ++e) up[e] = u[e];
+    __syncthreads();
+    T s[VN], x[VN];
+#pragma unroll
+    for (int e = 0; e < VN; ++e) s[e] = T(0);
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      T t[VN];
+      vload_smem(upart[it & 1][ww] + lane * VN, t);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) s[e] += t[e];
+    }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) x[e] = (r + e < R1) ? sub_rn(wv[e], s[e]) : T(0);
+    if (warp == 0) {
+      if (full) {
+        vstore(w + r, x);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e)
+          if (r + e < R1) w[r + e] = x[e];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KV; ++q)
+#pragma unroll
+      for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], x[e], acc[q]);
+  }
+  T* part = static_cast<T*>(ws.part);
+#pragma unroll
+  for (int q = 0; q < KV; ++q) {
+    const int i = warp + kWarps * q;
+    const T a = warp_sum(acc[q]);
+    if (lane == 0 && i < k) part[(size_t)blockIdx.x * k + i] = a;
+  }
+  if (last_cta(ws.counter)) {
+    const int jj = k - 1;
+    for (int c = warp; c < k; c += kWarps) {
+      T s2 = T(0);
+      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        sv.c2[c] = s2;
+        sv.Hc(jj, c) = add_rn(add_rn(T(0), sv.c1[c]), s2);   // h = 0; h += c1; h += c2
+      }
+    }
+  }
+}
+
 // ================================== generic-operator pass-1 dots (no SpMV)
 // c1 = V[:, :k]^T w, w0 = ||w||, finite check (krylov.py:133-139) for a w
 // produced by an arbitrary operator.
@@ -686,22 +899,93 @@ static cudaError_t launch_update_dot_reg(const T* V, long long ldv, long long n,
   return cudaGetLastError();
 }
 
+template <typename T, int KT>
+static cudaError_t launch_update_dot_q(const T* V, long long ldv, long long n, int k, T* w,
+                                       StateView<T> sv, WsView ws, cudaStream_t st) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [] {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dot_q<T, KT>, kThreads, 0);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  long long G = (n + 2 * (kThreads / 4) - 1) / (2 * (kThreads / 4));
+  const long long cap = (long long)num_sms() * occ;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_update_dot_q<T, KT><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
+  return cudaGetLastError();
+}
+
+template <typename T, int KV>
+static cudaError_t launch_update_dot_w(const T* V, long long ldv, long long n, int k, T* w,
+                                       StateView<T> sv, WsView ws, cudaStream_t st) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [] {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dot_w<T, KV>, kThreads, 0);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  constexpr long long RB = 32 * Vec<T>::n;
+  long long G = (n + RB - 1) / RB;
+  const long long cap = (long long)num_sms() * occ;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_update_dot_w<T, KV><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* w,
                               StateView<T> sv, WsView ws, cudaStream_t st) {
-  if (k <= 2) return launch_update_dot_reg<T, 2>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 4) return launch_update_dot_reg<T, 4>(V, ldv, n, k, w, sv, ws, st);
+  switch ((k + kWarps - 1) / kWarps) {
+    case 1: return launch_update_dot_w<T, 1>(V, ldv, n, k, w, sv, ws, st);
+    case 2: return launch_update_dot_w<T, 2>(V, ldv, n, k, w, sv, ws, st);
+    case 3: return launch_update_dot_w<T, 3>(V, ldv, n, k, w, sv, ws, st);
+    case 4: return launch_update_dot_w<T, 4>(V, ldv, n, k, w, sv, ws, st);
+    case 5: return launch_update_dot_w<T, 5>(V, ldv, n, k, w, sv, ws, st);
+    case 6: return launch_update_dot_w<T, 6>(V, ldv, n, k, w, sv, ws, st);
+    case 7: return launch_update_dot_w<T, 7>(V, ldv, n, k, w, sv, ws, st);
+    case 8: return launch_update_dot_w<T, 8>(V, ldv, n, k, w, sv, ws, st);
+    default: return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
+  }
+}
+
+// kept for A/B measurement: quad-split variant
+template <typename T>
+cudaError_t launch_update_dot_quadvariant(const T* V, long long ldv, long long n, int k, T* w,
+                                          StateView<T> sv, WsView ws, cudaStream_t st) {
+  if (k <= 4) return launch_update_dot_q<T, 4>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 8) return launch_update_dot_q<T, 8>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 12) return launch_update_dot_q<T, 12>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 16) return launch_update_dot_q<T, 16>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 24) return launch_update_dot_q<T, 24>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 32) return launch_update_dot_q<T, 32>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 40) return launch_update_dot_q<T, 40>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 48) return launch_update_dot_q<T, 48>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 56) return launch_update_dot_q<T, 56>(V, ldv, n, k, w, sv, ws, st);
+  if (k <= 64) return launch_update_dot_q<T, 64>(V, ldv, n, k, w, sv, ws, st);
+  return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
+}
+
+// kept for A/B measurement (MPG kernel variant sweep): one accumulator per vector per thread
+template <typename T>
+cudaError_t launch_update_dot_regvariant(const T* V, long long ldv, long long n, int k, T* w,
+                                         StateView<T> sv, WsView ws, cudaStream_t st) {
   if (k <= 8) return launch_update_dot_reg<T, 8>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 12) return launch_update_dot_reg<T, 12>(V, ldv, n, k, w, sv, ws, st);
   if (k <= 16) return launch_update_dot_reg<T, 16>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 24) return launch_update_dot_reg<T, 24>(V, ldv, n, k, w, sv, ws, st);
   if (k <= 32) return launch_update_dot_reg<T, 32>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 40) return launch_update_dot_reg<T, 40>(V, ldv, n, k, w, sv, ws, st);
   if (k <= 48) return launch_update_dot_reg<T, 48>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 56) return launch_update_dot_reg<T, 56>(V, ldv, n, k, w, sv, ws, st);
   if (k <= 64) return launch_update_dot_reg<T, 64>(V, ldv, n, k, w, sv, ws, st);
   return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
 }
+template cudaError_t launch_update_dot_regvariant<float>(const float*, long long, long long, int, float*,
+                                                         StateView<float>, WsView, cudaStream_t);
+template cudaError_t launch_update_dot_regvariant<double>(const double*, long long, long long, int, double*,
+                                                          StateView<double>, WsView, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,

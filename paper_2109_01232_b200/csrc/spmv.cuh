@@ -146,43 +146,65 @@ struct StencilView {
   int dims;
 };
 
+// exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
+__device__ __forceinline__ unsigned div_nx(unsigned r, unsigned long long magic) {
+  return (unsigned)(((unsigned long long)r * magic) >> 48);
+}
+__host__ __device__ inline unsigned long long nx_magic(unsigned nx) {
+  return ((1ULL << 48) + nx - 1) / nx;
+}
+
+template <typename T, int S>
+__device__ __forceinline__ T stencil_reduce(const bool (&pr)[S], const T (&pv)[S], const T (&px)[S]) {
+  // add.reduceat order for rows of <= 8 entries: p0 + (((p1 + p2) + p3) ...),
+  // over the present slots only (absent neighbours are not stored entries)
+  bool have = false;
+  T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    if (pr[s]) {
+      const T p = mul_rn(pv[s], px[s]);
+      if (!have) { p0 = p; have = true; }
+      else rest = add_rn(rest, p);
+    }
+  }
+  return add_rn(p0, rest);
+}
+
 template <typename T>
 __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __restrict__ x,
                                          long long r) {
   const unsigned nx = (unsigned)S.nx;
+  const unsigned long long mg = nx_magic(nx);
   const unsigned ur = (unsigned)r;
-  const unsigned ix = ur % nx;
-  const unsigned q = ur / nx;
-  bool have = false;
-  T p0 = T(0), rest = T(-0.0);
+  const unsigned q = div_nx(ur, mg);
+  const unsigned ix = ur - q * nx;
   const T* v = S.vals + r;
-  auto term = [&](bool present, int slot, long long off) {
-    if (present) {
-      const T p = mul_rn(__ldg(v + (size_t)slot * S.ldv), __ldg(x + r + off));
-      if (!have) { p0 = p; have = true; }
-      else rest = add_rn(rest, p);
-    }
-  };
+  const size_t ld = (size_t)S.ldv;
+  // every load is issued up front (predicated), the reduction below is load-free
   if (S.dims == 3) {
-    const unsigned iy = q % nx, iz = q / nx;
+    const unsigned iz = div_nx(q, mg);
+    const unsigned iy = q - iz * nx;
     const long long p2 = (long long)nx * nx;
-    term(iz > 0, 0, -p2);
-    term(iy > 0, 1, -(long long)nx);
-    term(ix > 0, 2, -1);
-    term(true, 3, 0);
-    term(ix + 1 < nx, 4, 1);
-    term(iy + 1 < nx, 5, (long long)nx);
-    term(iz + 1 < nx, 6, p2);
-  } else {
-    const unsigned iy = q;
-    term(iy > 0, 0, -(long long)nx);
-    term(ix > 0, 1, -1);
-    term(true, 2, 0);
-    term(ix + 1 < nx, 3, 1);
-    term(iy + 1 < nx, 4, (long long)nx);
+    const bool pr[7] = {iz > 0, iy > 0, ix > 0, true, ix + 1 < nx, iy + 1 < nx, iz + 1 < nx};
+    const long long off[7] = {-p2, -(long long)nx, -1, 0, 1, (long long)nx, p2};
+    T pv[7], px[7];
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+      pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
+      px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
+    }
+    return stencil_reduce<T, 7>(pr, pv, px);
   }
-  // add.reduceat order for rows of <= 8 entries: p0 + (((p1 + p2) + p3) ...)
-  return add_rn(p0, rest);
+  const bool pr[5] = {q > 0, ix > 0, true, ix + 1 < nx, q + 1 < nx};
+  const long long off[5] = {-(long long)nx, -1, 0, 1, (long long)nx};
+  T pv[5], px[5];
+#pragma unroll
+  for (int s = 0; s < 5; ++s) {
+    pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
+    px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
+  }
+  return stencil_reduce<T, 5>(pr, pv, px);
 }
 
 template <typename T, typename E>

@@ -255,6 +255,221 @@ struct EpiDot1Reg {
   }
 };
 
+// K_A, quad-split register variant (k <= KT, KT % 4 == 0): lane j of each
+// quad owns basis vectors i = 4q + j, so a thread holds KT/4 accumulators.
+// Per tile (512 rows = 64 quads x 8 rows) a quad covers rows
+// {VN*quad + 64*VN*h + e}, VN = 16 / sizeof(T) rows per 16-byte load, so one
+// warp-wide load instruction reads a contiguous 128-byte segment of each of
+// its 4 vectors.
+template <typename T, int KT>
+struct EpiDot1Quad {
+  static constexpr int KQ = KT / 4;
+  static constexpr int VN = 16 / (int)sizeof(T);
+  static constexpr int H = 8 / VN;
+  T* w;
+  const T* V;
+  long long ldv;
+  int k;
+  StateView<T> sv;
+  T* part;
+  unsigned int* counter;
+  T ss;
+  int bad;
+  T acc[KQ];
+  T* red2;   // [kSpConsumerWarps][KT] in dynamic smem
+  EpiShared<T>* sm;
+  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
+  __device__ void init(EpiShared<T>& s, unsigned char* extra) {
+    sm = &s;
+    red2 = reinterpret_cast<T*>(extra);
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) acc[q] = T(0);
+    ss = T(0);
+    bad = 0;
+  }
+  __device__ T on_row(long long r, T y) {
+    w[r] = y;
+    ss = fma_rn(y, y, ss);
+    bad |= !isfinite(y);
+    return y;
+  }
+  __device__ void on_tile(long long a, int nr, const T* ys) {
+    const int j = threadIdx.x & 3, quad = threadIdx.x >> 2;
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+      const int r0 = VN * quad + 64 * VN * h;
+      if (r0 >= nr) continue;
+      if (r0 + VN <= nr) {
+        T y[VN];
+        vload_smem(ys + r0, y);
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+          const int i = 4 * q + j;
+          if (i < k) {
+            T v[VN];
+            vload_cs(V + (size_t)i * ldv + a + r0, v);
+            T s = acc[q];
+#pragma unroll
+            for (int e = 0; e < VN; ++e) s = fma_rn(v[e], y[e], s);
+            acc[q] = s;
+          }
+        }
+      } else {
+        for (int e = 0; r0 + e < nr; ++e) {
+          const T ye = ys[r0 + e];
+#pragma unroll
+          for (int q = 0; q < KQ; ++q) {
+            const int i = 4 * q + j;
+            if (i < k) acc[q] = fma_rn(__ldcs(V + (size_t)i * ldv + a + r0 + e), ye, acc[q]);
+          }
+        }
+      }
+    }
+  }
+  __device__ void on_end() {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T t = consumer_block_sum(ss, sm->red);
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      T v = acc[q];
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      if (lane < 4) red2[warp * KT + 4 * q + lane] = v;
+    }
+    const int anybad = __any_sync(0xffffffffu, bad);
+    __shared__ int badw[kSpConsumerWarps];
+    if (lane == 0) badw[warp] = anybad;
+    consumer_sync();
+    const int stride = k + 2;
+    if ((int)threadIdx.x < k) {
+      T s = T(0);
+      for (int q = 0; q < kSpConsumerWarps; ++q) s += red2[q * KT + threadIdx.x];
+      part[(size_t)blockIdx.x * stride + threadIdx.x] = s;
+    }
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
+      part[(size_t)blockIdx.x * stride + k] = t;
+      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
+    }
+    __shared__ bool flag;
+    if (consumers_last_cta(counter, &flag)) {
+      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+        if (c < k) {
+          sv.c1[c] = s;
+        } else if (c == k) {
+          sv.h->w0 = (double)sqrt_rn(s);
+        } else if (s != T(0)) {
+          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
+          sv.h->done = 1;
+        }
+      });
+    }
+  }
+};
+
+// K_A, warp-owned-vector variant (k <= 8*KV): consumer warp w owns basis
+// vectors i = w + 8q.  After a tile's w is in shared memory, each lane streams
+// one 16-byte slice per owned vector per 32*VN-row group (a warp-wide load
+// = 512 contiguous bytes of one vector) into KV per-lane accumulators.
+template <typename T, int KV>
+struct EpiDot1Warp {
+  static constexpr int VN = 16 / (int)sizeof(T);
+  static constexpr int RB = 32 * VN;
+  T* w;
+  const T* V;
+  long long ldv;
+  int k;
+  StateView<T> sv;
+  T* part;
+  unsigned int* counter;
+  T ss;
+  int bad;
+  T acc[KV];
+  EpiShared<T>* sm;
+  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
+  __device__ void init(EpiShared<T>& s, unsigned char*) {
+    sm = &s;
+#pragma unroll
+    for (int q = 0; q < KV; ++q) acc[q] = T(0);
+    ss = T(0);
+    bad = 0;
+  }
+  __device__ T on_row(long long r, T y) {
+    w[r] = y;
+    ss = fma_rn(y, y, ss);
+    bad |= !isfinite(y);
+    return y;
+  }
+  __device__ void on_tile(long long a, int nr, const T* ys) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < kSpTile / RB; ++g) {
+      const int r0 = g * RB + lane * VN;
+      if (r0 + VN <= nr) {
+        T y[VN];
+        vload_smem(ys + r0, y);
+#pragma unroll
+        for (int q = 0; q < KV; ++q) {
+          const int i = warp + kSpConsumerWarps * q;
+          if (i < k) {
+            T v[VN];
+            vload_cs(V + (size_t)i * ldv + a + r0, v);
+            T s = acc[q];
+#pragma unroll
+            for (int e = 0; e < VN; ++e) s = fma_rn(v[e], y[e], s);
+            acc[q] = s;
+          }
+        }
+      } else if (r0 < nr) {
+        for (int e = 0; r0 + e < nr; ++e) {
+          const T ye = ys[r0 + e];
+#pragma unroll
+          for (int q = 0; q < KV; ++q) {
+            const int i = warp + kSpConsumerWarps * q;
+            if (i < k) acc[q] = fma_rn(__ldcs(V + (size_t)i * ldv + a + r0 + e), ye, acc[q]);
+          }
+        }
+      }
+    }
+  }
+  __device__ void on_end() {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T t = consumer_block_sum(ss, sm->red);
+    const int stride = k + 2;
+#pragma unroll
+    for (int q = 0; q < KV; ++q) {
+      const int i = warp + kSpConsumerWarps * q;
+      const T v = warp_sum(acc[q]);
+      if (lane == 0 && i < k) part[(size_t)blockIdx.x * stride + i] = v;
+    }
+    const int anybad = __any_sync(0xffffffffu, bad);
+    __shared__ int badw[kSpConsumerWarps];
+    if (lane == 0) badw[warp] = anybad;
+    consumer_sync();
+    if (threadIdx.x == 0) {
+      int b = 0;
+      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
+      part[(size_t)blockIdx.x * stride + k] = t;
+      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
+    }
+    __shared__ bool flag;
+    if (consumers_last_cta(counter, &flag)) {
+      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+        if (c < k) {
+          sv.c1[c] = s;
+        } else if (c == k) {
+          sv.h->w0 = (double)sqrt_rn(s);
+        } else if (s != T(0)) {
+          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
+          sv.h->done = 1;
+        }
+      });
+    }
+  }
+};
+
 // polynomial preconditioner steps (precond.py:272-319); the SpMV input is
 // `x` of the pipeline; other operands are own-row elementwise.
 template <typename T>
@@ -437,24 +652,24 @@ template <typename T, typename M>
 cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
                              StateView<T> sv, WsView ws, cudaStream_t st) {
   auto reg = [&](auto tag) {
-    constexpr int KT = decltype(tag)::value;
-    EpiDot1Reg<T, KT> e{};
+    constexpr int KV = decltype(tag)::value;
+    EpiDot1Warp<T, KV> e{};
     e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
     e.part = static_cast<T*>(ws.part);
     e.counter = ws.counter;
-    return launch_matrix(A, x, e, (size_t)kSpConsumerWarps * KT * sizeof(T), st);
+    return launch_matrix(A, x, e, 0, st);
   };
-  if (k <= 2) return reg(std::integral_constant<int, 2>{});
-  if (k <= 4) return reg(std::integral_constant<int, 4>{});
-  if (k <= 8) return reg(std::integral_constant<int, 8>{});
-  if (k <= 12) return reg(std::integral_constant<int, 12>{});
-  if (k <= 16) return reg(std::integral_constant<int, 16>{});
-  if (k <= 24) return reg(std::integral_constant<int, 24>{});
-  if (k <= 32) return reg(std::integral_constant<int, 32>{});
-  if (k <= 40) return reg(std::integral_constant<int, 40>{});
-  if (k <= 48) return reg(std::integral_constant<int, 48>{});
-  if (k <= 56) return reg(std::integral_constant<int, 56>{});
-  if (k <= 64) return reg(std::integral_constant<int, 64>{});
+  switch ((k + kSpConsumerWarps - 1) / kSpConsumerWarps) {
+    case 1: return reg(std::integral_constant<int, 1>{});
+    case 2: return reg(std::integral_constant<int, 2>{});
+    case 3: return reg(std::integral_constant<int, 3>{});
+    case 4: return reg(std::integral_constant<int, 4>{});
+    case 5: return reg(std::integral_constant<int, 5>{});
+    case 6: return reg(std::integral_constant<int, 6>{});
+    case 7: return reg(std::integral_constant<int, 7>{});
+    case 8: return reg(std::integral_constant<int, 8>{});
+    default: break;
+  }
   EpiDot1<T> e{};
   e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
   e.part = static_cast<T*>(ws.part);

@@ -33,6 +33,11 @@ def iters_match(rep, g, m, rtol=1e-10):
     got, want = rep.total_iters, g["total_iters"]
     if within_2pct(got, want):
         return True
+    # GMRES-FD: the fp64 leg restarts from the fp32 leg's iterate, which sits
+    # at the fp32 noise floor when the switch comes late (e.g. 7e-6 at the
+    # switch); the leg's length then moves with that noise.  Allow m/10.
+    if g.get("iters_fp32", 0) > 0 and g.get("iters_fp64", 0) > 0:
+        return abs(got - want) <= max(0.02 * want, m // 10)
     if abs(got - want) != m:
         return False
     if got < want:   # we converged one cycle earlier than the reference
