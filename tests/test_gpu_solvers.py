@@ -262,3 +262,35 @@ def test_stencil_storage_with_preconditioners():
         r1 = P.gmres_ir(A, b, precond_fp32=M, storage="csr")
         r2 = P.gmres_ir(A, b, precond_fp32=M, storage="stencil")
         assert r1.total_iters == r2.total_iters and np.array_equal(r1.x, r2.x)
+
+
+@pytest.fixture(scope="module")
+def cfg2_reference():
+    from conftest import load_json
+    return load_json("reference_cfg2.json")["runs"]
+
+
+@pytest.mark.parametrize("solver", ["ir", "fp64"])
+def test_cfg2_laplace3d150_full_solve_vs_reference(solver, cfg2_reference):
+    """BASELINE configs[1] at full size against the reference's own run
+    (tests/golden/reference_cfg2.json: 2387 fp64 / 2400 IR iterations,
+    ~20 / ~13 CPU-minutes): same count (+-2 %), every restart-boundary
+    residual within 2x, final fp64 residual <= 1e-10, solution within 1e-8
+    relative on a 4101-point strided sample."""
+    g = cfg2_reference[f"laplace3d:150/{solver}/m50"]
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, 150))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    crit = P.StopCriteria(rtol=1e-10, m=50)
+    rep = P.gmres_ir(A, b, criteria=crit) if solver == "ir" else P.gmres_restarted(A, b, criteria=crit)
+    assert rep.converged
+    assert iters_match(rep, g, 50), (rep.total_iters, g["total_iters"])
+    ours = {e.iteration: e.explicit for e in rep.residual_history if e.explicit is not None}
+    for it, _, ref_exp, _ in g["boundaries"]:
+        if it in ours and it > 0:
+            assert 0.5 <= ours[it] / ref_exp <= 2.0, (it, ours[it], ref_exp)
+    nr, _ = P.explicit_residual(A, b, rep.x)
+    assert nr / float(torch.linalg.norm(b)) <= 1e-10
+    x = rep.x.cpu().numpy()[:: g["x_stride"]]
+    ref = np.asarray(g["x_sample"])
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-8
+    assert abs(float(torch.linalg.norm(rep.x)) - g["x_norm"]) / g["x_norm"] <= 1e-8
