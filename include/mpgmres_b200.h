@@ -131,6 +131,12 @@ int mpg_generate_stencil(int kind, int64_t nx, double convection, double stretch
 int mpg_stencil_pack(int prec, int dims, int64_t nx, int64_t n, const int32_t* row_ptr,
                      const int32_t* col_idx, const void* values, void* dia, int64_t ldv,
                      int32_t* bad, void* stream);
+/* Same for rows [row0, row0 + nrows) of the global stencil (a rank's block):
+ * row_ptr relative to row0 (row_ptr[0] = 0), global col_idx, as produced by
+ * mpg_generate_stencil for that range.  dia is [S][ldv] over local rows. */
+int mpg_stencil_pack_rows(int prec, int dims, int64_t nx, int64_t row0, int64_t nrows,
+                          const int32_t* row_ptr, const int32_t* col_idx, const void* values,
+                          void* dia, int64_t ldv, int32_t* bad, void* stream);
 /* y = A x from the packed storage; bit-identical to mpg_spmv on the CSR. */
 int mpg_spmv_dia(int prec, int dims, int64_t nx, int64_t n, const void* dia, int64_t ldv,
                  const void* x, void* y, void* ws, void* stream);
@@ -279,7 +285,34 @@ typedef struct {
   const void* dia;        /* slot-major values, working precision, stride ldv */
   const double* dia64;    /* IR: fp64 values for the outer residual */
   const void* pc_dia;     /* poly preconditioner: values in pc_prec */
+  /* row-partitioned (distributed) mode, driven phase by phase through
+   * mpg_solver_phase with the caller's collectives in between */
+  int32_t dist;           /* 1: this handle is one rank of a row partition */
+  int32_t reserved_i;
+  int64_t row0;           /* global index of local row 0 */
+  int64_t halo;           /* halo rows stored on each side of every V row and of x */
 } mpg_solver_desc;
+
+/* Phases of one distributed restart cycle.  A phase marked
+ * "raw" leaves this rank's partial sums in the state (red[] in the working
+ * precision, or header reserved[0] as a double) for the caller to allreduce
+ * (sum) before the matching POST phase; "halo" phases read the halo planes
+ * of their input vector, which the caller exchanges beforehand. */
+#define MPG_PH_BNORM 0        /* raw: sum b^2 -> reserved[0]                       */
+#define MPG_PH_POST_BNORM 1
+#define MPG_PH_RESID 2        /* halo(x); raw: local sum r^2 -> reserved[0]        */
+#define MPG_PH_POST_RESID 3
+#define MPG_PH_START 4        /* raw: gamma^2 (+ IR overflow) -> red[0..2)         */
+#define MPG_PH_POST_START 5
+#define MPG_PH_START_SCALE 6
+#define MPG_PH_SPMV_DOT 7     /* halo(V[:,j]); raw: c1, w0^2, nonfinite -> red[0..j+3) */
+#define MPG_PH_POST_DOT1 8
+#define MPG_PH_UPDATE_DOT 9   /* raw: c2 -> red[0..j+1)                            */
+#define MPG_PH_POST_DOT2 10
+#define MPG_PH_UPDATE_NORM 11 /* raw: ||w||^2 -> red[0]                            */
+#define MPG_PH_POST_NORM 12
+#define MPG_PH_SCALE 13
+#define MPG_PH_FINISH 14      /* back-solve (replicated) + local solution update   */
 
 typedef struct mpg_solver mpg_solver;
 
@@ -300,6 +333,9 @@ int mpg_solver_cycle(mpg_solver* s, int32_t m_limit, void* stream);
  * 6 back-solve + solution update, 7 explicit residual. */
 int mpg_solver_profile_cycle(mpg_solver* s, int32_t m_limit, void* stream, double* ms_out,
                              int32_t* launches_out);
+/* Enqueue one phase of a distributed cycle (desc.dist = 1); j = Arnoldi
+ * step, m_limit = the cycle's step budget. */
+int mpg_solver_phase(mpg_solver* s, int32_t phase, int32_t j, int32_t m_limit, void* stream);
 
 #ifdef __cplusplus
 }

@@ -61,7 +61,9 @@ class SolverDesc(C.Structure):
                 ("pc_t0", C.c_void_p), ("pc_t1", C.c_void_p), ("pc_t2", C.c_void_p),
                 ("pc_t3", C.c_void_p), ("pc_t4", C.c_void_p),
                 ("stencil_dims", C.c_int32), ("stencil_nx", C.c_int32),
-                ("dia", C.c_void_p), ("dia64", C.c_void_p), ("pc_dia", C.c_void_p)]
+                ("dia", C.c_void_p), ("dia64", C.c_void_p), ("pc_dia", C.c_void_p),
+                ("dist", C.c_int32), ("reserved_i", C.c_int32), ("row0", C.c_int64),
+                ("halo", C.c_int64)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -81,6 +83,9 @@ _SIGS = {
     "mpg_generate_stencil": (C.c_int, [C.c_int, _i64, _d, _d, _i64, _i64, _vp, _vp, _vp, _vp]),
     "mpg_stencil_pack": (C.c_int, [C.c_int, C.c_int, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "mpg_spmv_dia": (C.c_int, [C.c_int, C.c_int, _i64, _i64, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "mpg_stencil_pack_rows": (C.c_int, [C.c_int, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp,
+                                        _i64, _vp, _vp]),
+    "mpg_solver_phase": (C.c_int, [_vp, _i32, _i32, _i32, _vp]),
     "mpg_jacobi_apply": (C.c_int, [C.c_int, _i64, _i32, _vp, _vp, _vp, _vp, _vp]),
     "mpg_jacobi_build": (C.c_int, [C.c_int, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mpg_poly_apply": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, C.POINTER(PolyOp), _i32, _vp, _vp,

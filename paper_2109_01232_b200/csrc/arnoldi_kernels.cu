@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kUdThreads) k_update_dot(const T* __restrict__
       for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
       s2 = warp_sum(s2);
       if (lane == 0) {
+        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
         sv.c2[c] = s2;
         // h = 0; h += c1; h += c2  (krylov.py:137-141)
         sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_reg(const T* __restrict
       for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
       s2 = warp_sum(s2);
       if (lane == 0) {
+        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
         sv.c2[c] = s2;
         sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
       }
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_q(const T* __restrict__
       for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
       s2 = warp_sum(s2);
       if (lane == 0) {
+        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
         sv.c2[c] = s2;
         sv.Hc(jj, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
       }
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
       for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
       s2 = warp_sum(s2);
       if (lane == 0) {
+        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
         sv.c2[c] = s2;
         sv.Hc(jj, c) = add_rn(add_rn(T(0), sv.c1[c]), s2);   // h = 0; h += c1; h += c2
       }
@@ -623,6 +627,7 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ 
     for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
     s = block_sum(s, red);
     if (threadIdx.x == 0) {
+      if (sv.dist) { sv.red[0] = s; return; }   // raw local sum (distributed)
       const T hs = sqrt_rn(s);
       sv.Hc(j, j + 1) = hs;
       sv.h->h_sub = (double)hs;
@@ -715,6 +720,10 @@ __global__ void __launch_bounds__(kThreads) k_start(const T* __restrict__ r0, lo
     // restarted cycles threshold on the outer ||b|| (solvers.py:186,198);
     // a null source means "use gamma" (gmres_cycle with b_norm=None, r0=b)
     const double bn = b_norm_src ? *b_norm_src : -1.0;
+    if (sv.dist) {                   // raw local sum; k_dist_post initialises
+      if (threadIdx.x == 0) sv.red[0] = s;
+      return;
+    }
     init_state(sv, gamma, bn, rtol, btol, 0);
   }
 }
@@ -754,8 +763,12 @@ __global__ void __launch_bounds__(kThreads) k_start_ir(const double* __restrict_
     o = block_sum(o, red);
     const float gamma = sqrt_rn(s);
     // the inner cycle's b_norm is ||r32|| itself (solvers.py:146 with b = r32)
-    init_state(sv, gamma, -1.0, rtol, btol, o > 0.f ? MPG_FLAG_OVERFLOW : 0);
     if (threadIdx.x == 0) sv.h->rho = rho;
+    if (sv.dist) {                   // raw local sums; k_dist_post initialises
+      if (threadIdx.x == 0) { sv.red[0] = s; sv.red[1] = o; }
+      return;
+    }
+    init_state(sv, gamma, -1.0, rtol, btol, o > 0.f ? MPG_FLAG_OVERFLOW : 0);
   }
 }
 
@@ -768,6 +781,80 @@ __global__ void __launch_bounds__(kThreads) k_start_scale(const T* __restrict__ 
        i += (long long)gridDim.x * blockDim.x)
     v0[i] = div_rn(r0[i], gamma);
 }
+
+// ======================================================= distributed: post
+// After the allreduce of a phase's raw local sums (red[] or reserved[0]),
+// one CTA finishes the phase exactly as the single-GPU last CTA would: the
+// derived scalars, the Hessenberg column and the Givens rotation are computed
+// from bitwise-identical inputs on every rank, so the replicated small state
+// stays identical across ranks.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_dist_post(int phase, StateView<T> sv, int j,
+                                                        int m_limit, double rtol, double btol,
+                                                        int flag) {
+  mpg_state_header* h = sv.h;
+  switch (phase) {
+    case DP_POST_START: {   // flag: 1 = IR (b_norm = gamma, overflow flag in red[1])
+      const T gamma = sqrt_rn(sv.red[0]);
+      const int f = (flag && sv.red[1] > T(0)) ? MPG_FLAG_OVERFLOW : 0;
+      init_state(sv, gamma, flag ? -1.0 : h->outer_b_norm, rtol, btol, f);
+      return;
+    }
+    case DP_POST_DOT1: {
+      if (gated(h)) return;
+      const int k = j + 1;
+      for (int c = threadIdx.x; c < k; c += blockDim.x) sv.c1[c] = sv.red[c];
+      if (threadIdx.x == 0) {
+        h->w0 = (double)sqrt_rn(sv.red[k]);
+        if (sv.red[k + 1] != T(0)) {
+          h->flags |= MPG_FLAG_NONFINITE_OP;
+          h->done = 1;
+        }
+      }
+      return;
+    }
+    case DP_POST_DOT2: {
+      if (gated(h)) return;
+      const int k = j + 1;
+      for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        sv.c2[c] = sv.red[c];
+        sv.Hc(j, c) = add_rn(add_rn(T(0), sv.c1[c]), sv.red[c]);   // h = 0; h += c1; h += c2
+      }
+      return;
+    }
+    case DP_POST_NORM: {
+      if (gated(h)) return;
+      if (threadIdx.x == 0) {
+        const T hs = sqrt_rn(sv.red[0]);
+        sv.Hc(j, j + 1) = hs;
+        h->h_sub = (double)hs;
+        const bool brk = (double)hs <= h->breakdown_tol * h->w0;
+        givens_column(sv, j, h->threshold, brk, m_limit);
+      }
+      return;
+    }
+    case DP_POST_RESID:     // flag: 1 = the outer precision is fp64
+      if (threadIdx.x == 0)
+        h->rnorm = flag ? __dsqrt_rn(h->reserved[0]) : (double)__fsqrt_rn((float)h->reserved[0]);
+      return;
+    case DP_POST_BNORM:
+      if (threadIdx.x == 0)
+        h->outer_b_norm = flag ? __dsqrt_rn(h->reserved[0]) : (double)__fsqrt_rn((float)h->reserved[0]);
+      return;
+    default:
+      return;
+  }
+}
+
+template <typename T>
+cudaError_t launch_dist_post(int phase, StateView<T> sv, int j, int m_limit, double rtol,
+                             double btol, int flag, cudaStream_t st) {
+  count_launch();
+  k_dist_post<T><<<1, kThreads, 0, st>>>(phase, sv, j, m_limit, rtol, btol, flag);
+  return cudaGetLastError();
+}
+template cudaError_t launch_dist_post<float>(int, StateView<float>, int, int, double, double, int, cudaStream_t);
+template cudaError_t launch_dist_post<double>(int, StateView<double>, int, int, double, double, int, cudaStream_t);
 
 // ======================================================================= lsq
 // Back-substitution R[:k,:k] d = g[:k] (krylov.py:190-202; LAPACK xTRSV 'U','N'

@@ -129,17 +129,27 @@ static int stencil_shape_ok(int dims, int64_t nx, int64_t n) {
   return n == (dims == 3 ? nx * nx * nx : nx * nx) && n < (1LL << 32);
 }
 
+int mpg_stencil_pack_rows(int prec, int dims, int64_t nx, int64_t row0, int64_t nrows,
+                          const int32_t* rp, const int32_t* ci, const void* v, void* dia,
+                          int64_t ldv, int32_t* bad, void* stream) {
+  const int64_t N = dims == 3 ? nx * nx * nx : nx * nx;
+  if (!stencil_shape_ok(dims, nx, N) || row0 < 0 || nrows < 1 || row0 + nrows > N || ldv < nrows ||
+      !rp || !dia || !bad)
+    return MPG_EARG;
+  if (prec == MPG_FP64)
+    return rc(launch_stencil_pack<double>(dims, (int)nx, row0, nrows, rp, ci, (const double*)v,
+                                          (double*)dia, ldv, bad, S(stream)));
+  if (prec == MPG_FP32)
+    return rc(launch_stencil_pack<float>(dims, (int)nx, row0, nrows, rp, ci, (const float*)v,
+                                         (float*)dia, ldv, bad, S(stream)));
+  return MPG_EARG;
+}
+
 int mpg_stencil_pack(int prec, int dims, int64_t nx, int64_t n, const int32_t* rp,
                      const int32_t* ci, const void* v, void* dia, int64_t ldv, int32_t* bad,
                      void* stream) {
-  if (!stencil_shape_ok(dims, nx, n) || ldv < n || !rp || !dia || !bad) return MPG_EARG;
-  if (prec == MPG_FP64)
-    return rc(launch_stencil_pack<double>(dims, (int)nx, n, rp, ci, (const double*)v, (double*)dia,
-                                          ldv, bad, S(stream)));
-  if (prec == MPG_FP32)
-    return rc(launch_stencil_pack<float>(dims, (int)nx, n, rp, ci, (const float*)v, (float*)dia, ldv,
-                                         bad, S(stream)));
-  return MPG_EARG;
+  if (!stencil_shape_ok(dims, nx, n)) return MPG_EARG;
+  return mpg_stencil_pack_rows(prec, dims, nx, 0, n, rp, ci, v, dia, ldv, bad, stream);
 }
 
 int mpg_spmv_dia(int prec, int dims, int64_t nx, int64_t n, const void* dia, int64_t ldv,
@@ -147,10 +157,10 @@ int mpg_spmv_dia(int prec, int dims, int64_t nx, int64_t n, const void* dia, int
   if (!stencil_shape_ok(dims, nx, n) || ldv < n || !dia || !ws) return MPG_EARG;
   WsView w = make_ws(ws);
   if (prec == MPG_FP64)
-    return rc(launch_spmv<double>(StencilView<double>{(const double*)dia, ldv, n, (int)nx, dims},
+    return rc(launch_spmv<double>(StencilView<double>{(const double*)dia, ldv, n, (int)nx, dims, 0},
                                   (const double*)x, (double*)y, w, S(stream)));
   if (prec == MPG_FP32)
-    return rc(launch_spmv<float>(StencilView<float>{(const float*)dia, ldv, n, (int)nx, dims},
+    return rc(launch_spmv<float>(StencilView<float>{(const float*)dia, ldv, n, (int)nx, dims, 0},
                                  (const float*)x, (float*)y, w, S(stream)));
   return MPG_EARG;
 }
@@ -216,8 +226,8 @@ int64_t mpg_state_bytes(int prec, int32_t m) {
 
 int64_t mpg_state_offset(int prec, int32_t m, int32_t which) {
   StateLayout L = state_layout(prec, m);
-  const int64_t offs[9] = {L.H, L.R, L.cs, L.sn, L.g, L.c1, L.c2, L.d, L.implicit};
-  if (which < 0 || which > 8) return -1;
+  const int64_t offs[10] = {L.H, L.R, L.cs, L.sn, L.g, L.c1, L.c2, L.d, L.implicit, L.red};
+  if (which < 0 || which > 9) return -1;
   return offs[which];
 }
 

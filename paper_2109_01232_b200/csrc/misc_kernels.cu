@@ -22,7 +22,7 @@ __device__ __forceinline__ bool gate_done(const mpg_state_header* h) {
 // ============================================================ norm2 (core.py:341-354)
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_norm2(const T* __restrict__ x, long long n,
-                                                    double* out, WsView ws) {
+                                                    double* out, WsView ws, int raw) {
   __shared__ T red[32];
   T ss = T(0);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kThreads) k_norm2(const T* __restrict__ x, lon
     T s = T(0);
     for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
     s = block_sum(s, red);
-    if (threadIdx.x == 0) *out = (double)sqrt_rn(s);
+    if (threadIdx.x == 0) *out = raw ? (double)s : (double)sqrt_rn(s);   // raw: distributed sum
   }
 }
 
@@ -380,9 +380,9 @@ __global__ void __launch_bounds__(kThreads) k_generate(int kind, long long nx, d
 // ================================================================= launchers
 
 template <typename T>
-cudaError_t launch_norm2(const T* x, long long n, double* out, WsView ws, cudaStream_t st) {
+cudaError_t launch_norm2(const T* x, long long n, double* out, WsView ws, cudaStream_t st, int raw) {
   count_launch();
-  k_norm2<T><<<grid_for_rows(n, 4), kThreads, 0, st>>>(x, n, out, ws);
+  k_norm2<T><<<grid_for_rows(n, 4), kThreads, 0, st>>>(x, n, out, ws, raw);
   return cudaGetLastError();
 }
 
@@ -507,7 +507,7 @@ long long host_nnz_before(int kind, long long nx, long long r) {
 }
 
 #define INST(T)                                                                                  \
-  template cudaError_t launch_norm2<T>(const T*, long long, double*, WsView, cudaStream_t);     \
+  template cudaError_t launch_norm2<T>(const T*, long long, double*, WsView, cudaStream_t, int); \
   template cudaError_t launch_gemv_t<T>(const T*, long long, long long, int, const T*, T*, T, T, \
                                         WsView, cudaStream_t);                                 \
   template cudaError_t launch_gemv_n<T>(const T*, long long, long long, int, const T*, T*, T, T, \

@@ -85,7 +85,8 @@ template <typename TP, typename F>
 static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, const void* dia,
                                F&& f) {
   if (d.stencil_dims && dia)
-    return f(StencilView<TP>{static_cast<const TP*>(dia), d.ldv, d.n, d.stencil_nx, d.stencil_dims});
+    return f(StencilView<TP>{static_cast<const TP*>(dia), d.ldv, d.n, d.stencil_nx, d.stencil_dims,
+                             d.row0});
   return f(CsrView<TP>{d.row_ptr, d.col_idx, csr_vals, d.n});
 }
 
@@ -244,6 +245,78 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   return outer_residual(d, ws, st);
 }
 
+// One phase of a distributed cycle (MPG_PH_*): the same kernels in dist mode
+// (raw local sums) plus the 1-CTA post kernels; collectives are the caller's.
+template <typename T>
+static cudaError_t enqueue_phase(const mpg_solver& s, int phase, int j, int m_limit,
+                                 cudaStream_t st) {
+  const mpg_solver_desc& d = s.d;
+  StateView<T> sv = make_state<T>(d.state, d.m);
+  sv.dist = 1;
+  WsView ws = make_ws(d.ws);
+  T* V = static_cast<T*>(d.V);
+  T* w = static_cast<T*>(d.w);
+  mpg_state_header* h = hdr_of(d);
+  const bool ir = d.mode == MPG_MODE_IR;
+  const bool outer64 = ir || d.prec == MPG_FP64;
+  switch (phase) {
+    case MPG_PH_BNORM:
+      return outer64 ? launch_norm2<double>(static_cast<const double*>(d.b), d.n, &h->reserved[0], ws, st, 1)
+                     : launch_norm2<float>(static_cast<const float*>(d.b), d.n, &h->reserved[0], ws, st, 1);
+    case MPG_PH_POST_BNORM:
+      return launch_dist_post<T>(DP_POST_BNORM, sv, 0, 0, d.rtol, d.breakdown_tol, outer64, st);
+    case MPG_PH_RESID:
+      if (outer64) {
+        const void* dia = ir ? static_cast<const void*>(d.dia64) : d.dia;
+        const double* vals = ir ? d.values64 : static_cast<const double*>(d.values);
+        return with_matrix<double>(d, vals, dia, [&](const auto& A) {
+          return launch_residual<double>(A, static_cast<const double*>(d.b),
+                                         static_cast<const double*>(d.x), static_cast<double*>(d.r),
+                                         nullptr, h, ws, st, 1);
+        });
+      }
+      return with_matrix<float>(d, static_cast<const float*>(d.values), d.dia, [&](const auto& A) {
+        return launch_residual<float>(A, static_cast<const float*>(d.b), static_cast<const float*>(d.x),
+                                      static_cast<float*>(d.r), nullptr, h, ws, st, 1);
+      });
+    case MPG_PH_POST_RESID:
+      return launch_dist_post<T>(DP_POST_RESID, sv, 0, 0, d.rtol, d.breakdown_tol, outer64, st);
+    case MPG_PH_START:
+      if (ir) {
+        if constexpr (sizeof(T) == 4)
+          return launch_start_ir(static_cast<const double*>(d.r), static_cast<float*>(d.r_in), d.n, sv,
+                                 d.rtol, d.breakdown_tol, ws, st);
+        return cudaErrorInvalidValue;
+      }
+      return launch_start<T>(static_cast<const T*>(d.r), d.n, sv, d.rtol, &h->outer_b_norm,
+                             d.breakdown_tol, ws, st);
+    case MPG_PH_POST_START:
+      return launch_dist_post<T>(DP_POST_START, sv, 0, 0, d.rtol, d.breakdown_tol, ir ? 1 : 0, st);
+    case MPG_PH_START_SCALE:
+      return launch_start_scale<T>(static_cast<const T*>(ir ? d.r_in : d.r), V, d.n, sv, st);
+    case MPG_PH_SPMV_DOT:
+      return with_matrix<T>(d, static_cast<const T*>(d.values), d.dia, [&](const auto& A) {
+        return launch_spmv_dot1<T>(A, V + (size_t)j * d.ldv, w, V, d.ldv, j + 1, sv, ws, st);
+      });
+    case MPG_PH_POST_DOT1:
+      return launch_dist_post<T>(DP_POST_DOT1, sv, j, m_limit, d.rtol, d.breakdown_tol, 0, st);
+    case MPG_PH_UPDATE_DOT:
+      return launch_update_dot<T>(V, d.ldv, d.n, j + 1, w, sv, ws, st);
+    case MPG_PH_POST_DOT2:
+      return launch_dist_post<T>(DP_POST_DOT2, sv, j, m_limit, d.rtol, d.breakdown_tol, 0, st);
+    case MPG_PH_UPDATE_NORM:
+      return launch_update_norm<T>(V, d.ldv, d.n, j, w, sv, ws, m_limit, st);
+    case MPG_PH_POST_NORM:
+      return launch_dist_post<T>(DP_POST_NORM, sv, j, m_limit, d.rtol, d.breakdown_tol, 0, st);
+    case MPG_PH_SCALE:
+      return launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st);
+    case MPG_PH_FINISH:
+      return finish_cycle<T>(s, sv, ws, st);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
 static cudaError_t enqueue_any(const mpg_solver& s, int m_limit, cudaStream_t st) {
   return s.d.prec == MPG_FP64 ? enqueue_cycle<double>(s, m_limit, st)
                               : enqueue_cycle<float>(s, m_limit, st);
@@ -264,7 +337,10 @@ extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) 
   if (d.stencil_dims) {
     if ((d.stencil_dims != 2 && d.stencil_dims != 3) || d.stencil_nx < 2 || !d.dia) return MPG_EARG;
     const long long nx = d.stencil_nx;
-    if (d.n != (d.stencil_dims == 3 ? nx * nx * nx : nx * nx) || d.n >= (1LL << 32)) return MPG_EARG;
+    const long long N = d.stencil_dims == 3 ? nx * nx * nx : nx * nx;
+    if (N >= (1LL << 32)) return MPG_EARG;
+    if (!d.dist && d.n != N) return MPG_EARG;
+    if (d.dist && (d.row0 < 0 || d.row0 + d.n > N)) return MPG_EARG;
     if (d.mode == MPG_MODE_IR && !d.dia64) return MPG_EARG;
     if (d.pc_kind == MPG_PC_POLY && !d.pc_dia) return MPG_EARG;
   }
@@ -275,6 +351,7 @@ extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) 
     if (d.pc_kind == MPG_PC_POLY && (!d.pc_ops || d.pc_nops < 1 || !d.pc_values)) return MPG_EARG;
     if (!d.pc_t0 || !d.pc_t1) return MPG_EARG;
   }
+  if (d.dist && (!d.stencil_dims || d.pc_kind != MPG_PC_NONE)) return MPG_EUNSUPPORTED;
   mpg_solver* s = new mpg_solver();
   s->d = d;
   if (d.pc_kind == MPG_PC_POLY) s->ops.assign(d.pc_ops, d.pc_ops + d.pc_nops);
@@ -335,6 +412,15 @@ extern "C" int mpg_solver_cycle(mpg_solver* s, int32_t m_limit, void* stream) {
   cudaError_t e = cudaGraphLaunch(it->second, st);
   if (e == cudaSuccess) count_launch(s->graph_launches[m_limit]);
   return (int)e;
+}
+
+extern "C" int mpg_solver_phase(mpg_solver* s, int32_t phase, int32_t j, int32_t m_limit,
+                                void* stream) {
+  if (!s || !s->d.dist) return MPG_ESTATE;
+  if (j < 0 || j >= s->d.m || m_limit < 1 || m_limit > s->d.m) return MPG_EARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return (int)(s->d.prec == MPG_FP64 ? enqueue_phase<double>(*s, phase, j, m_limit, st)
+                                     : enqueue_phase<float>(*s, phase, j, m_limit, st));
 }
 
 extern "C" int mpg_solver_profile_cycle(mpg_solver* s, int32_t m_limit, void* stream,

@@ -137,6 +137,10 @@ __device__ __forceinline__ void tile_dots(int k, int nr, const VRow& vrow, const
 // a zero), so each row is reduced over exactly the CSR row's entries, in the
 // same order: bit-identical to the CSR kernel and to the reference.
 // Traffic per row drops from nnz_row*(s+4)+4 bytes to S*s bytes of values.
+// vals/x are indexed by LOCAL row r in [0, n); grid coordinates come from the
+// global row r + row0 (row-partitioned ranks).  x may be read at r + off
+// outside [0, n): the halo planes a distributed caller stores around the
+// owned block (csrc/solver.cu, distributed mode).
 template <typename T>
 struct StencilView {
   const T* vals;
@@ -144,6 +148,7 @@ struct StencilView {
   long long n;
   int nx;
   int dims;
+  long long row0;
 };
 
 // exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
@@ -176,7 +181,7 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
                                          long long r) {
   const unsigned nx = (unsigned)S.nx;
   const unsigned long long mg = nx_magic(nx);
-  const unsigned ur = (unsigned)r;
+  const unsigned ur = (unsigned)(r + S.row0);
   const unsigned q = div_nx(ur, mg);
   const unsigned ix = ur - q * nx;
   const T* v = S.vals + r;

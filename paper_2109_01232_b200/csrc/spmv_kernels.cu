@@ -60,6 +60,7 @@ struct EpiResid {
   mpg_state_header* hdr;
   T* part;
   unsigned int* counter;
+  int raw;
   T ss;
   EpiShared<T>* sm;
   __device__ bool skip() const { return false; }
@@ -77,6 +78,10 @@ struct EpiResid {
     __shared__ bool flag;
     if (consumers_last_cta(counter, &flag)) {
       consumers_finalize(part, gridDim.x, 1, 1, [&](int, T s) {
+        if (raw) {                  // distributed: local sum of squares, finished after the allreduce
+          hdr->reserved[0] = (double)s;
+          return;
+        }
         const double nr = (double)sqrt_rn(s);
         if (out) *out = nr;
         if (hdr) hdr->rnorm = nr;
@@ -136,227 +141,9 @@ struct EpiDot1 {
     __shared__ bool flag;
     if (consumers_last_cta(counter, &flag)) {
       consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
-        if (c < k) {
-          sv.c1[c] = s;
-        } else if (c == k) {
-          sv.h->w0 = (double)sqrt_rn(s);
-        } else if (s != T(0)) {
-          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
-          sv.h->done = 1;
-        }
-      });
-    }
-  }
-};
-
-// K_A, register variant for k <= KT: the thread that computes w_r also
-// accumulates V[i][r] * w_r into KT per-thread accumulators (coalesced
-// across the warp), so the pass-1 dots need no shared-memory tile phase.
-// One CTA-level reduction of the accumulators at the end.
-template <typename T, int KT>
-struct EpiDot1Reg {
-  T* w;
-  const T* V;
-  long long ldv;
-  int k;
-  StateView<T> sv;
-  T* part;
-  unsigned int* counter;
-  T ss;
-  int bad;
-  T acc[KT];
-  T* red2;   // [kSpConsumerWarps][KT] in dynamic smem
-  EpiShared<T>* sm;
-  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
-  __device__ void init(EpiShared<T>& s, unsigned char* extra) {
-    sm = &s;
-    red2 = reinterpret_cast<T*>(extra);
-#pragma unroll
-    for (int i = 0; i < KT; ++i) acc[i] = T(0);
-    ss = T(0);
-    bad = 0;
-  }
-  __device__ T on_row(long long r, T y) {
-    w[r] = y;
-    ss = fma_rn(y, y, ss);
-    bad |= !isfinite(y);
-    return y;
-  }
-  // After the tile's w is complete in shared memory: thread t owns tile rows
-  // [2t, 2t+2) and streams that 2-row slice of every basis vector with
-  // back-to-back 8/16-byte loads (k independent loads in flight per thread).
-  __device__ void on_tile(long long a, int nr, const T* ys) {
-    const int rr = 2 * (int)threadIdx.x;
-    if (kSpTile < 2 * kSpConsumers && rr >= kSpTile) return;
-    if (rr + 1 < nr) {
-      const T y0 = ys[rr], y1 = ys[rr + 1];
-      const T* v = V + a + rr;
-#pragma unroll
-      for (int i = 0; i < KT; ++i) {
-        if (i < k) {
-          T q0, q1;
-          if constexpr (sizeof(T) == 4) {
-            const float2 q = __ldcs(reinterpret_cast<const float2*>(v + (size_t)i * ldv));
-            q0 = q.x; q1 = q.y;
-          } else {
-            const double2 q = __ldcs(reinterpret_cast<const double2*>(v + (size_t)i * ldv));
-            q0 = q.x; q1 = q.y;
-          }
-          acc[i] = fma_rn(q1, y1, fma_rn(q0, y0, acc[i]));
-        }
-      }
-    } else if (rr < nr) {
-      const T y0 = ys[rr];
-      const T* v = V + a + rr;
-#pragma unroll
-      for (int i = 0; i < KT; ++i)
-        if (i < k) acc[i] = fma_rn(__ldcs(v + (size_t)i * ldv), y0, acc[i]);
-    }
-  }
-  __device__ void on_end() {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T t = consumer_block_sum(ss, sm->red);
-#pragma unroll
-    for (int i = 0; i < KT; ++i) {
-      if (i < k) {
-        const T a = warp_sum(acc[i]);
-        if (lane == 0) red2[warp * KT + i] = a;
-      }
-    }
-    const int anybad = __any_sync(0xffffffffu, bad);
-    __shared__ int badw[kSpConsumerWarps];
-    if (lane == 0) badw[warp] = anybad;
-    consumer_sync();
-    const int stride = k + 2;
-    if ((int)threadIdx.x < k) {
-      T s = T(0);
-      for (int q = 0; q < kSpConsumerWarps; ++q) s += red2[q * KT + threadIdx.x];
-      part[(size_t)blockIdx.x * stride + threadIdx.x] = s;
-    }
-    if (threadIdx.x == 0) {
-      int b = 0;
-      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
-      part[(size_t)blockIdx.x * stride + k] = t;
-      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
-    }
-    __shared__ bool flag;
-    if (consumers_last_cta(counter, &flag)) {
-      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
-        if (c < k) {
-          sv.c1[c] = s;
-        } else if (c == k) {
-          sv.h->w0 = (double)sqrt_rn(s);
-        } else if (s != T(0)) {
-          sv.h->flags |= MPG_FLAG_NONFINITE_OP;
-          sv.h->done = 1;
-        }
-      });
-    }
-  }
-};
-
-// K_A, quad-split register variant (k <= KT, KT % 4 == 0): lane j of each
-// quad owns basis vectors i = 4q + j, so a thread holds KT/4 accumulators.
-// Per tile (512 rows = 64 quads x 8 rows) a quad covers rows
-// {VN*quad + 64*VN*h + e}, VN = 16 / sizeof(T) rows per 16-byte load, so one
-// warp-wide load instruction reads a contiguous 128-byte segment of each of
-// its 4 vectors.
-template <typename T, int KT>
-struct EpiDot1Quad {
-  static constexpr int KQ = KT / 4;
-  static constexpr int VN = 16 / (int)sizeof(T);
-  static constexpr int H = 8 / VN;
-  T* w;
-  const T* V;
-  long long ldv;
-  int k;
-  StateView<T> sv;
-  T* part;
-  unsigned int* counter;
-  T ss;
-  int bad;
-  T acc[KQ];
-  T* red2;   // [kSpConsumerWarps][KT] in dynamic smem
-  EpiShared<T>* sm;
-  __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
-  __device__ void init(EpiShared<T>& s, unsigned char* extra) {
-    sm = &s;
-    red2 = reinterpret_cast<T*>(extra);
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) acc[q] = T(0);
-    ss = T(0);
-    bad = 0;
-  }
-  __device__ T on_row(long long r, T y) {
-    w[r] = y;
-    ss = fma_rn(y, y, ss);
-    bad |= !isfinite(y);
-    return y;
-  }
-  __device__ void on_tile(long long a, int nr, const T* ys) {
-    const int j = threadIdx.x & 3, quad = threadIdx.x >> 2;
-#pragma unroll
-    for (int h = 0; h < H; ++h) {
-      const int r0 = VN * quad + 64 * VN * h;
-      if (r0 >= nr) continue;
-      if (r0 + VN <= nr) {
-        T y[VN];
-        vload_smem(ys + r0, y);
-#pragma unroll
-        for (int q = 0; q < KQ; ++q) {
-          const int i = 4 * q + j;
-          if (i < k) {
-            T v[VN];
-            vload_cs(V + (size_t)i * ldv + a + r0, v);
-            T s = acc[q];
-#pragma unroll
-            for (int e = 0; e < VN; ++e) s = fma_rn(v[e], y[e], s);
-            acc[q] = s;
-          }
-        }
-      } else {
-        for (int e = 0; r0 + e < nr; ++e) {
-          const T ye = ys[r0 + e];
-#pragma unroll
-          for (int q = 0; q < KQ; ++q) {
-            const int i = 4 * q + j;
-            if (i < k) acc[q] = fma_rn(__ldcs(V + (size_t)i * ldv + a + r0 + e), ye, acc[q]);
-          }
-        }
-      }
-    }
-  }
-  __device__ void on_end() {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T t = consumer_block_sum(ss, sm->red);
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      T v = acc[q];
-      v += __shfl_xor_sync(0xffffffffu, v, 4);
-      v += __shfl_xor_sync(0xffffffffu, v, 8);
-      v += __shfl_xor_sync(0xffffffffu, v, 16);
-      if (lane < 4) red2[warp * KT + 4 * q + lane] = v;
-    }
-    const int anybad = __any_sync(0xffffffffu, bad);
-    __shared__ int badw[kSpConsumerWarps];
-    if (lane == 0) badw[warp] = anybad;
-    consumer_sync();
-    const int stride = k + 2;
-    if ((int)threadIdx.x < k) {
-      T s = T(0);
-      for (int q = 0; q < kSpConsumerWarps; ++q) s += red2[q * KT + threadIdx.x];
-      part[(size_t)blockIdx.x * stride + threadIdx.x] = s;
-    }
-    if (threadIdx.x == 0) {
-      int b = 0;
-      for (int i = 0; i < kSpConsumerWarps; ++i) b |= badw[i];
-      part[(size_t)blockIdx.x * stride + k] = t;
-      part[(size_t)blockIdx.x * stride + k + 1] = b ? T(1) : T(0);
-    }
-    __shared__ bool flag;
-    if (consumers_last_cta(counter, &flag)) {
-      consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
-        if (c < k) {
+        if (sv.dist) {
+          sv.red[c] = s;
+        } else if (c < k) {
           sv.c1[c] = s;
         } else if (c == k) {
           sv.h->w0 = (double)sqrt_rn(s);
@@ -457,7 +244,9 @@ struct EpiDot1Warp {
     __shared__ bool flag;
     if (consumers_last_cta(counter, &flag)) {
       consumers_finalize(part, gridDim.x, stride, k + 2, [&](int c, T s) {
-        if (c < k) {
+        if (sv.dist) {              // raw local sums; k_dist_post finishes after the allreduce
+          sv.red[c] = s;
+        } else if (c < k) {
           sv.c1[c] = s;
         } else if (c == k) {
           sv.h->w0 = (double)sqrt_rn(s);
@@ -539,14 +328,15 @@ __global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, cons
 // DIA packing + pattern check: one thread per row.  *bad != 0 when the CSR
 // pattern is not exactly the Dirichlet 5/7-point stencil of the grid.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, long long n,
+__global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, long long row0, long long n,
                                                            const int32_t* __restrict__ rp,
                                                            const int32_t* __restrict__ ci,
                                                            const T* __restrict__ v, T* out,
                                                            long long ldv, int* bad) {
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
        r += (long long)gridDim.x * blockDim.x) {
-    const unsigned unx = (unsigned)nx, ur = (unsigned)r;
+    const long long rg = r + row0;   // global row (row_ptr local, col_idx global)
+    const unsigned unx = (unsigned)nx, ur = (unsigned)rg;
     const unsigned ix = ur % unx, q = ur / unx;
     bool pres[7];
     long long off[7];
@@ -576,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, lon
     for (int sl = 0; sl < S; ++sl) {
       T val = T(0);
       if (pres[sl]) {
-        if (p < e && (long long)ci[p] == r + off[sl]) val = v[p++];
+        if (p < e && (long long)ci[p] == rg + off[sl]) val = v[p++];
         else ok = 0;
       }
       out[(size_t)sl * ldv + r] = val;
@@ -640,9 +430,9 @@ cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView, cudaStream_t st) {
 
 template <typename T, typename M>
 cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
-                            mpg_state_header* hdr, WsView ws, cudaStream_t st) {
+                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw) {
   EpiResid<T> e{};
-  e.b = b; e.r = r; e.out = norm_out; e.hdr = hdr;
+  e.b = b; e.r = r; e.out = norm_out; e.hdr = hdr; e.raw = raw;
   e.part = static_cast<T*>(ws.part);
   e.counter = ws.counter;
   return launch_matrix(A, x, e, 0, st);
@@ -695,20 +485,21 @@ cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, 
 }
 
 template <typename T>
-cudaError_t launch_stencil_pack(int dims, int nx, long long n, const int32_t* rp, const int32_t* ci,
-                                const T* v, T* out, long long ldv, int* bad, cudaStream_t st) {
+cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, const int32_t* rp,
+                                const int32_t* ci, const T* v, T* out, long long ldv, int* bad,
+                                cudaStream_t st) {
   long long G = (n + kThreads - 1) / kThreads;
   if (G > (long long)num_sms() * 8) G = (long long)num_sms() * 8;
   if (G < 1) G = 1;
   count_launch();
-  k_stencil_pack<T><<<(unsigned)G, kThreads, 0, st>>>(dims, nx, n, rp, ci, v, out, ldv, bad);
+  k_stencil_pack<T><<<(unsigned)G, kThreads, 0, st>>>(dims, nx, row0, n, rp, ci, v, out, ldv, bad);
   return cudaGetLastError();
 }
 
 #define INST_M(T, M)                                                                            \
   template cudaError_t launch_spmv<T, M>(const M&, const T*, T*, WsView, cudaStream_t);         \
   template cudaError_t launch_residual<T, M>(const M&, const T*, const T*, T*, double*,         \
-                                             mpg_state_header*, WsView, cudaStream_t);         \
+                                             mpg_state_header*, WsView, cudaStream_t, int);    \
   template cudaError_t launch_spmv_dot1<T, M>(const M&, const T*, T*, const T*, long long, int, \
                                               StateView<T>, WsView, cudaStream_t);             \
   template cudaError_t launch_poly_op<T, M>(const M&, const mpg_poly_op&, const T*, T*, T*, T*, \
@@ -719,9 +510,11 @@ INST_M(double, CsrView<double>)
 INST_M(float, StencilView<float>)
 INST_M(double, StencilView<double>)
 #undef INST_M
-template cudaError_t launch_stencil_pack<float>(int, int, long long, const int32_t*, const int32_t*,
-                                                const float*, float*, long long, int*, cudaStream_t);
-template cudaError_t launch_stencil_pack<double>(int, int, long long, const int32_t*, const int32_t*,
-                                                 const double*, double*, long long, int*, cudaStream_t);
+template cudaError_t launch_stencil_pack<float>(int, int, long long, long long, const int32_t*,
+                                                const int32_t*, const float*, float*, long long, int*,
+                                                cudaStream_t);
+template cudaError_t launch_stencil_pack<double>(int, int, long long, long long, const int32_t*,
+                                                 const int32_t*, const double*, double*, long long,
+                                                 int*, cudaStream_t);
 
 }  // namespace mpg

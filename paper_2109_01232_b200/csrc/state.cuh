@@ -8,7 +8,7 @@ namespace mpg {
 
 // ------------------------------------------------------------------ state
 struct StateLayout {
-  int64_t implicit, H, R, cs, sn, g, c1, c2, d, total;
+  int64_t implicit, H, R, cs, sn, g, c1, c2, d, red, total;
 };
 
 inline __host__ __device__ int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
@@ -26,6 +26,7 @@ inline __host__ __device__ StateLayout state_layout(int prec, int m) {
   L.c1 = off; off = align_up(off + s * (m + 1), 64);
   L.c2 = off; off = align_up(off + s * (m + 1), 64);
   L.d = off; off = align_up(off + s * (m + 1), 64);
+  L.red = off; off = align_up(off + s * (m + 8), 64);   // raw per-rank sums (distributed mode)
   L.total = off;
   return L;
 }
@@ -34,8 +35,9 @@ template <typename T>
 struct StateView {
   mpg_state_header* h;
   double* implicit;
-  T *H, *R, *cs, *sn, *g, *c1, *c2, *d;
+  T *H, *R, *cs, *sn, *g, *c1, *c2, *d, *red;
   int m;
+  int dist;   // 1: kernels publish raw local sums to red[] for a cross-rank allreduce
   __device__ __forceinline__ T& Hc(int col, int row) const { return H[(size_t)col * (m + 1) + row]; }
   __device__ __forceinline__ T& Rc(int col, int row) const { return R[(size_t)col * (m + 1) + row]; }
 };
@@ -56,7 +58,9 @@ inline StateView<T> make_state(void* base, int m) {
   s.c1 = reinterpret_cast<T*>(b + L.c1);
   s.c2 = reinterpret_cast<T*>(b + L.c2);
   s.d = reinterpret_cast<T*>(b + L.d);
+  s.red = reinterpret_cast<T*>(b + L.red);
   s.m = m;
+  s.dist = 0;
   return s;
 }
 
@@ -91,7 +95,7 @@ template <typename T, typename M>
 cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView ws, cudaStream_t st);
 template <typename T, typename M>
 cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
-                            mpg_state_header* hdr, WsView ws, cudaStream_t st);
+                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw = 0);
 template <typename T, typename M>
 cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
                              StateView<T> sv, WsView ws, cudaStream_t st);
@@ -100,8 +104,9 @@ cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, 
                            T* t2, const mpg_state_header* gate, long long n, WsView ws,
                            cudaStream_t st);
 template <typename T>
-cudaError_t launch_stencil_pack(int dims, int nx, long long n, const int32_t* rp, const int32_t* ci,
-                                const T* v, T* out, long long ldv, int* bad, cudaStream_t st);
+cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, const int32_t* rp,
+                                const int32_t* ci, const T* v, T* out, long long ldv, int* bad,
+                                cudaStream_t st);
 
 // arnoldi family (arnoldi_kernels.cu)
 template <typename T>
@@ -128,6 +133,19 @@ cudaError_t launch_start_scale(const T* r0, T* v0, long long n, StateView<T> sv,
 template <typename T>
 cudaError_t launch_lsq(StateView<T> sv, cudaStream_t st);
 
+// distributed-mode post phases (k_dist_post)
+enum DistPostPhase {
+  DP_POST_START = 0,
+  DP_POST_DOT1 = 1,
+  DP_POST_DOT2 = 2,
+  DP_POST_NORM = 3,
+  DP_POST_RESID = 4,
+  DP_POST_BNORM = 5,
+};
+template <typename T>
+cudaError_t launch_dist_post(int phase, StateView<T> sv, int j, int m_limit, double rtol,
+                             double btol, int flag, cudaStream_t st);
+
 enum CombineMode {
   CMB_STORE = 0,    // u = V d
   CMB_ADD = 1,      // x += V d
@@ -142,7 +160,8 @@ cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> 
 
 // misc (misc_kernels.cu)
 template <typename T>
-cudaError_t launch_norm2(const T* x, long long n, double* out, WsView ws, cudaStream_t st);
+cudaError_t launch_norm2(const T* x, long long n, double* out, WsView ws, cudaStream_t st,
+                         int raw = 0);
 template <typename T>
 cudaError_t launch_gemv_t(const T* A, long long lda, long long rows, int cols, const T* x, T* y,
                           T alpha, T beta, WsView ws, cudaStream_t st);
