@@ -255,6 +255,85 @@ def native_arm(args, rank: int, world: int):
     return out
 
 
+def _backend() -> str:
+    return os.environ.get("MPG_BENCH_BACKEND", "nccl")
+
+
+def dist_arm(args, rank: int, world: int):
+    """--gpus N > 1: the same cfg2 GMRES-IR solve row-partitioned over N GPUs
+    (one process per GPU, NCCL halo exchange + allreduces), strong scaling."""
+    import numpy as np
+    import torch
+
+    import paper_2109_01232_b200 as P
+    from paper_2109_01232_b200 import _lib
+    from paper_2109_01232_b200.dist import Collectives, DistributedStencilSolver, RowPartition, _dist_solve
+    from paper_2109_01232_b200.solvers import StopCriteria
+
+    from paper_2109_01232_b200.dist import HostStagedCollectives
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+    spec = P.StencilSpec(P.StencilKind.LAPLACE3D, NX)
+    part = RowPartition.for_stencil(3, NX, world, rank)
+    # NCCL (device collectives) on the multi-GPU box; gloo only for smoke runs
+    # of this path with several ranks sharing one GPU (MPG_BENCH_BACKEND=gloo)
+    coll = HostStagedCollectives() if _backend() == "gloo" else Collectives()
+    crit = StopCriteria(rtol=RTOL, m=M)
+    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll)
+
+    def solve():
+        solver.x_buf.zero_()
+        return _dist_solve(solver, crit, True, None)
+
+    for _ in range(args.warmup):
+        rep = solve()
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    l0 = _lib.launch_count()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            rep = solve()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - l0
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    solve_s = float(t.item()) / args.steps
+    # e2e: public distributed API with a host right-hand side slice, x downloaded
+    b_host = np.ones(part.n_local)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    from paper_2109_01232_b200.dist import dist_gmres_ir
+    rep_h = dist_gmres_ir(spec, part, coll, crit, b_local=b_host)
+    x_host = rep_h.x.cpu().numpy()
+    torch.cuda.synchronize()
+    e2e = torch.tensor([time.perf_counter() - t0], device="cuda")
+    torch.distributed.all_reduce(e2e, op=torch.distributed.ReduceOp.MAX)
+    solver.close()
+    return {
+        "metric": METRIC, "value": round(solve_s, 5), "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(solve_s * 1e3, 3),
+        "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": round(solve_s / PUBLISHED_V100_IR_S, 5),
+        "vs_baseline_note": "value / published V100 GMRES-IR time 11.75 s (PAPER.md:461)",
+        "dtype": "f32 inner / f64 outer", "data": "synthetic (per-rank device assembly); b = ones, x0 = 0",
+        "config": {"workload": "gmres_ir laplace3d:150 GMRES(50) rtol=1e-10 (BASELINE configs[1]), "
+                               "row-partitioned by z-planes",
+                   "n": NX ** 3, "m": M, "rtol": RTOL, "parallelism": f"rows{world}",
+                   "collectives": "NCCL halo send/recv + 3 allreduces per Arnoldi step",
+                   "l2": "working set >> L2 per rank at N<=8; no flush needed"},
+        "iters": rep.total_iters, "iters_reference": REFERENCE_IR_ITERS,
+        "storage": "stencil", "gpu_launches": launches, "clocks": clk.summary(),
+        "roofline": None,
+        "e2e": {"value": round(float(e2e.item()), 5), "unit": "s",
+                "h2d_bytes_per_step": int(b_host.nbytes) * world, "d2h_bytes_per_step": int(x_host.nbytes) * world,
+                "iters": rep_h.total_iters},
+    }
+
+
 def cpu_sample(threads: int | None):
     """Oracle GMRES-IR at the bench config: one outer cycle (50 fp32 inner
     iterations + the fp64 residual), extrapolated to the reference's 2400
@@ -310,8 +389,11 @@ def main():
         return
     if world > 1:
         import torch
-        torch.distributed.init_process_group("nccl")
-    out = native_arm(args, rank, world)
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)) % torch.cuda.device_count())
+        torch.distributed.init_process_group(_backend())
+        out = dist_arm(args, rank, world)
+    else:
+        out = native_arm(args, rank, world)
     if rank == 0:
         if not args.no_cpu_baseline:
             v, dt = cpu_sample(1)
