@@ -903,10 +903,42 @@ __global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, l
   __syncthreads();
   const double rho = sv.h->rho;
   int bad = 0;
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
-       r += (long long)gridDim.x * blockDim.x) {
-    T acc = T(0);
-    for (int i = 0; i < k; ++i) acc = fma_rn(__ldcs(V + (size_t)i * ldv + r), ds[i], acc);
+  // 16-byte vector loads over VN consecutive rows (k independent loads in flight)
+  constexpr int VN = Vec<T>::n;
+  const long long nv = n / VN;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < nv + (n - nv * VN); g += stride) {
+    T accv[VN];
+    long long r0;
+    int cnt;
+    if (g < nv) {
+      r0 = g * VN;
+      cnt = VN;
+#pragma unroll
+      for (int e = 0; e < VN; ++e) accv[e] = T(0);
+      int i = 0;
+      for (; i + 2 <= k; i += 2) {
+        T a[VN], b[VN];
+        vload_cs(V + (size_t)i * ldv + r0, a);
+        vload_cs(V + (size_t)(i + 1) * ldv + r0, b);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) accv[e] = fma_rn(b[e], ds[i + 1], fma_rn(a[e], ds[i], accv[e]));
+      }
+      for (; i < k; ++i) {
+        T a[VN];
+        vload_cs(V + (size_t)i * ldv + r0, a);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) accv[e] = fma_rn(a[e], ds[i], accv[e]);
+      }
+    } else {
+      r0 = nv * VN + (g - nv);
+      cnt = 1;
+      accv[0] = T(0);
+      for (int i = 0; i < k; ++i) accv[0] = fma_rn(__ldcs(V + (size_t)i * ldv + r0), ds[i], accv[0]);
+    }
+    for (int e = 0; e < cnt; ++e) {
+    const long long r = r0 + e;
+    const T acc = accv[e];
     if constexpr (MODE == CMB_STORE) {
       u[r] = acc;
     } else if constexpr (MODE == CMB_ADD) {
@@ -925,6 +957,7 @@ __global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, l
       const float a32 = __double2float_rn((double)acc);
       const float y = __fdiv_rn(a32, static_cast<const float*>(diag)[r]);
       x[r] = __dadd_rn((double)x[r], (double)y);
+    }
     }
   }
   if (bad) atomicOr(&sv.h->flags, MPG_FLAG_NONFINITE_X);
@@ -1166,7 +1199,7 @@ cudaError_t launch_lsq(StateView<T> sv, cudaStream_t st) {
 template <typename T>
 cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> sv, int mode,
                            void* x, const void* diag, T* u, cudaStream_t st) {
-  const unsigned G = grid_stream(n);
+  const unsigned G = grid_stream((n + Vec<T>::n - 1) / Vec<T>::n, 6);
   const size_t smem = (size_t)(sv.m + 1) * sizeof(T);
   count_launch();
   switch (mode) {

@@ -225,19 +225,37 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
     TRY(launch_start_scale<T>(static_cast<const T*>(d.r), V, d.n, sv, st));
   }
   }
+  // Without a preconditioner the basis scaling V[:, j] = w / h_sub (krylov.py:148)
+  // is folded into step j's SpMV: it gathers w / h with the same IEEE division
+  // and writes V[:, j] for its own rows, so w ping-pongs between two buffers.
+  // Measured on B200 (cfg2): the 7 IEEE divisions per row cost more than the separate
+  // 10 us scaling launch saves, so the fused variant stays off (kept for A/B runs).
+  const bool fuse = false && d.pc_kind == MPG_PC_NONE && d.m <= 64;
+  T* wbuf[2] = {w, fuse ? static_cast<T*>(d.u) : w};
   for (int j = 0; j < m_limit; ++j) {
-    const T* vj = V + (size_t)j * d.ldv;
-    const T* z = nullptr;
-    { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
-    {
+    T* wj = wbuf[j & 1];
+    if (fuse && j > 0) {
+      ProfScope ps(PK_SPMV_DOT);
+      const T* hprev = sv.H + (size_t)(j - 1) * (d.m + 1) + j;   // H[j, j-1] = h_sub of step j-1
+      TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
+        return launch_spmv_dot1<T>(A, wbuf[(j - 1) & 1], wj, V, d.ldv, j + 1, sv, ws, st, hprev,
+                                   V + (size_t)j * d.ldv);
+      }));
+    } else {
+      const T* vj = V + (size_t)j * d.ldv;
+      const T* z = nullptr;
+      { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
       ProfScope ps(PK_SPMV_DOT);
       TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
-        return launch_spmv_dot1<T>(A, z, w, V, d.ldv, j + 1, sv, ws, st);
+        return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
       }));
     }
-    { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, w, sv, ws, st)); }
-    { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, w, sv, ws, m_limit, st)); }
-    { ProfScope ps(PK_SCALE); TRY(launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st)); }
+    { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, wj, sv, ws, st)); }
+    { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, wj, sv, ws, m_limit, st)); }
+    if (!fuse) {
+      ProfScope ps(PK_SCALE);
+      TRY(launch_step_scale<T>(wj, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st));
+    }
   }
   { ProfScope ps(PK_FINISH); TRY(finish_cycle<T>(s, sv, ws, st)); }
   ProfScope ps(PK_RESIDUAL);

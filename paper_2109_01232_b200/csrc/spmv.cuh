@@ -35,7 +35,16 @@ struct CsrView {
   const int32_t* ci;
   const T* v;
   long long n;
+  // fused basis scaling (stencil path only; see StencilView)
+  const T* xdiv = nullptr;
 };
+
+// x_c, or x_c / h when the SpMV consumes an unscaled basis vector
+template <typename T>
+__device__ __forceinline__ T xload(const T* __restrict__ x, long long c, bool scaled, T h) {
+  const T v = __ldg(x + c);
+  return scaled ? div_rn(v, h) : v;
+}
 
 // shared memory the epilogues use (tile of SpMV results + reduction scratch)
 template <typename T>
@@ -149,6 +158,7 @@ struct StencilView {
   int nx;
   int dims;
   long long row0;
+  const T* xdiv = nullptr;   // fused basis scaling (see CsrView)
 };
 
 // exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
@@ -176,9 +186,9 @@ __device__ __forceinline__ T stencil_reduce(const bool (&pr)[S], const T (&pv)[S
   return add_rn(p0, rest);
 }
 
-template <typename T>
+template <typename T, bool scaled = false>
 __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __restrict__ x,
-                                         long long r) {
+                                         long long r, T hdiv = T(1)) {
   const unsigned nx = (unsigned)S.nx;
   const unsigned long long mg = nx_magic(nx);
   const unsigned ur = (unsigned)(r + S.row0);
@@ -197,7 +207,7 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
 #pragma unroll
     for (int s = 0; s < 7; ++s) {
       pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
-      px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
+      px[s] = pr[s] ? (scaled ? div_rn(__ldg(x + r + off[s]), hdiv) : __ldg(x + r + off[s])) : T(0);
     }
     return stencil_reduce<T, 7>(pr, pv, px);
   }
@@ -207,7 +217,7 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
-    px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
+    px[s] = pr[s] ? (scaled ? div_rn(__ldg(x + r + off[s]), hdiv) : __ldg(x + r + off[s])) : T(0);
   }
   return stencil_reduce<T, 5>(pr, pv, px);
 }
@@ -217,12 +227,19 @@ __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const 
                                                  E& epi, EpiShared<T>& es) {
   long long R0, R1;
   cta_rows(S.n, R0, R1);
+  const bool scaled = S.xdiv != nullptr;
+  const T hdiv = scaled ? __ldg(S.xdiv) : T(1);
   int t = 0;
   for (long long a = R0; a < R1; a += kSpTile, ++t) {
     const int nrows = (int)min((long long)kSpTile, R1 - a);
     T* ys = es.ys[t & 1];
-    for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
-      ys[rr] = epi.on_row(a + rr, stencil_row(S, x, a + rr));
+    if (scaled) {
+      for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
+        ys[rr] = epi.on_row(a + rr, stencil_row<T, true>(S, x, a + rr, hdiv));
+    } else {
+      for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
+        ys[rr] = epi.on_row(a + rr, stencil_row<T, false>(S, x, a + rr));
+    }
     consumer_sync();
     epi.on_tile(a, nrows, ys);
   }

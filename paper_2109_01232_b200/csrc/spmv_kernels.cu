@@ -175,6 +175,11 @@ struct EpiDot1Warp {
   int bad;
   T acc[KV];
   EpiShared<T>* sm;
+  // fused basis scaling (K_S folded in): V[:, j] = x / h for this CTA's rows
+  const T* vsrc;
+  T* vout;
+  const T* hsrc;
+  T hval;
   __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
   __device__ void init(EpiShared<T>& s, unsigned char*) {
     sm = &s;
@@ -182,8 +187,10 @@ struct EpiDot1Warp {
     for (int q = 0; q < KV; ++q) acc[q] = T(0);
     ss = T(0);
     bad = 0;
+    hval = hsrc ? __ldg(hsrc) : T(1);
   }
   __device__ T on_row(long long r, T y) {
+    if (vout) vout[r] = div_rn(vsrc[r], hval);   // krylov.py:148, same IEEE division
     w[r] = y;
     ss = fma_rn(y, y, ss);
     bad |= !isfinite(y);
@@ -439,16 +446,21 @@ cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* no
 }
 
 template <typename T, typename M>
-cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
-                             StateView<T> sv, WsView ws, cudaStream_t st) {
+cudaError_t launch_spmv_dot1(const M& A0, const T* x, T* w, const T* V, long long ldv, int k,
+                             StateView<T> sv, WsView ws, cudaStream_t st, const T* xdiv,
+                             T* vout) {
+  M A = A0;
+  A.xdiv = xdiv;
   auto reg = [&](auto tag) {
     constexpr int KV = decltype(tag)::value;
     EpiDot1Warp<T, KV> e{};
     e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
     e.part = static_cast<T*>(ws.part);
     e.counter = ws.counter;
+    e.vsrc = x; e.vout = xdiv ? vout : nullptr; e.hsrc = xdiv;
     return launch_matrix(A, x, e, 0, st);
   };
+  if (xdiv && k > 8 * kSpConsumerWarps) return cudaErrorInvalidValue;   // fused scaling: k <= 64
   switch ((k + kSpConsumerWarps - 1) / kSpConsumerWarps) {
     case 1: return reg(std::integral_constant<int, 1>{});
     case 2: return reg(std::integral_constant<int, 2>{});
@@ -501,7 +513,8 @@ cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, c
   template cudaError_t launch_residual<T, M>(const M&, const T*, const T*, T*, double*,         \
                                              mpg_state_header*, WsView, cudaStream_t, int);    \
   template cudaError_t launch_spmv_dot1<T, M>(const M&, const T*, T*, const T*, long long, int, \
-                                              StateView<T>, WsView, cudaStream_t);             \
+                                              StateView<T>, WsView, cudaStream_t, const T*,    \
+                                              T*);                                             \
   template cudaError_t launch_poly_op<T, M>(const M&, const mpg_poly_op&, const T*, T*, T*, T*, \
                                             T*, const mpg_state_header*, long long, WsView,    \
                                             cudaStream_t);
