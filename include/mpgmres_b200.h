@@ -290,7 +290,10 @@ typedef struct {
   int32_t dist;           /* 1: this handle is one rank of a row partition */
   int32_t reserved_i;
   int64_t row0;           /* global index of local row 0 */
-  int64_t halo;           /* halo rows stored on each side of every V row and of x */
+  int64_t halo;           /* readable rows on each side of every SpMV input (V rows, x,
+                             preconditioner buffers): the distributed halo, or zero padding
+                             on one GPU; >= one grid plane enables the branchless stencil rows */
+  int64_t dia_ld;         /* slot stride of dia/dia64/pc_dia (0: same as ldv) */
 } mpg_solver_desc;
 
 /* Phases of one distributed restart cycle.  A phase marked

@@ -63,7 +63,7 @@ class SolverDesc(C.Structure):
                 ("stencil_dims", C.c_int32), ("stencil_nx", C.c_int32),
                 ("dia", C.c_void_p), ("dia64", C.c_void_p), ("pc_dia", C.c_void_p),
                 ("dist", C.c_int32), ("reserved_i", C.c_int32), ("row0", C.c_int64),
-                ("halo", C.c_int64)]
+                ("halo", C.c_int64), ("dia_ld", C.c_int64)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double

@@ -84,9 +84,13 @@ static cudaError_t outer_residual(const mpg_solver_desc& d, WsView ws, cudaStrea
 template <typename TP, typename F>
 static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, const void* dia,
                                F&& f) {
-  if (d.stencil_dims && dia)
-    return f(StencilView<TP>{static_cast<const TP*>(dia), d.ldv, d.n, d.stencil_nx, d.stencil_dims,
-                             d.row0});
+  if (d.stencil_dims && dia) {
+    StencilView<TP> S{static_cast<const TP*>(dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
+                      d.stencil_dims, d.row0};
+    const long long plane = d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx : d.stencil_nx;
+    S.padded = d.halo >= plane ? 1 : 0;
+    return f(S);
+  }
   return f(CsrView<TP>{d.row_ptr, d.col_idx, csr_vals, d.n});
 }
 

@@ -159,7 +159,64 @@ struct StencilView {
   int dims;
   long long row0;
   const T* xdiv = nullptr;   // fused basis scaling (see CsrView)
+  // 1: every SpMV input has >= one grid plane of readable padding (or halo)
+  // on both sides, so rows use the branchless sentinel path below
+  int padded = 0;
 };
+
+// Absent stencil slots (neighbour outside the grid) hold this NaN payload in
+// the packed values; arithmetic never produces it (generated NaNs are quiet,
+// canonical), so presence can be read off the loaded value.
+__host__ __device__ constexpr unsigned kAbsent32 = 0x7fa5a5a5u;
+__host__ __device__ constexpr unsigned long long kAbsent64 = 0x7ff4a5a5a5a5a5a5ull;
+__device__ __forceinline__ bool present(float v) { return __float_as_uint(v) != kAbsent32; }
+__device__ __forceinline__ bool present(double v) {
+  return (unsigned long long)__double_as_longlong(v) != kAbsent64;
+}
+template <typename T> __host__ __device__ inline T absent_value();
+template <> __host__ __device__ inline float absent_value<float>() {
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(kAbsent32);
+#else
+  float f; unsigned u = kAbsent32; __builtin_memcpy(&f, &u, 4); return f;
+#endif
+}
+template <> __host__ __device__ inline double absent_value<double>() {
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double((long long)kAbsent64);
+#else
+  double d; unsigned long long u = kAbsent64; __builtin_memcpy(&d, &u, 8); return d;
+#endif
+}
+
+// Branchless row on padded inputs: all S value loads and S neighbour loads
+// are unconditional (absent slots read padding / the sentinel), then the
+// add.reduceat order p0 + (((p1 + p2) + p3) ...) over the present slots is
+// applied with selects.  No grid coordinates are needed.
+template <typename T, int S, bool scaled>
+__device__ __forceinline__ T stencil_row_padded(const T* __restrict__ v, size_t ld,
+                                                const T* __restrict__ xr, const long long (&off)[S],
+                                                T hdiv) {
+  T pv[S], px[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    pv[s] = __ldg(v + s * ld);
+    px[s] = __ldg(xr + off[s]);
+  }
+  bool have = false;
+  T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const T xs = scaled ? div_rn(px[s], hdiv) : px[s];
+    const T p = mul_rn(pv[s], xs);
+    const bool pr = present(pv[s]);
+    const T nrest = add_rn(rest, p);
+    rest = (pr && have) ? nrest : rest;
+    p0 = (pr && !have) ? p : p0;
+    have = have || pr;
+  }
+  return add_rn(p0, rest);
+}
 
 // exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
 __device__ __forceinline__ unsigned div_nx(unsigned r, unsigned long long magic) {
@@ -222,6 +279,20 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
   return stencil_reduce<T, 5>(pr, pv, px);
 }
 
+template <typename T, typename E, typename RowF>
+__device__ __forceinline__ void stencil_loop(long long R0, long long R1, E& epi, EpiShared<T>& es,
+                                             const RowF& rowf) {
+  int t = 0;
+  for (long long a = R0; a < R1; a += kSpTile, ++t) {
+    const int nrows = (int)min((long long)kSpTile, R1 - a);
+    T* ys = es.ys[t & 1];
+    for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers) ys[rr] = epi.on_row(a + rr, rowf(a + rr));
+    consumer_sync();
+    epi.on_tile(a, nrows, ys);
+  }
+  epi.on_end();
+}
+
 template <typename T, typename E>
 __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
                                                  E& epi, EpiShared<T>& es) {
@@ -229,21 +300,25 @@ __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const 
   cta_rows(S.n, R0, R1);
   const bool scaled = S.xdiv != nullptr;
   const T hdiv = scaled ? __ldg(S.xdiv) : T(1);
-  int t = 0;
-  for (long long a = R0; a < R1; a += kSpTile, ++t) {
-    const int nrows = (int)min((long long)kSpTile, R1 - a);
-    T* ys = es.ys[t & 1];
-    if (scaled) {
-      for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
-        ys[rr] = epi.on_row(a + rr, stencil_row<T, true>(S, x, a + rr, hdiv));
+  const size_t ld = (size_t)S.ldv;
+  if (S.padded && !scaled) {
+    const long long nx = S.nx, p2 = nx * nx;
+    if (S.dims == 3) {
+      const long long off[7] = {-p2, -nx, -1, 0, 1, nx, p2};
+      stencil_loop(R0, R1, epi, es, [&](long long r) {
+        return stencil_row_padded<T, 7, false>(S.vals + r, ld, x + r, off, hdiv);
+      });
     } else {
-      for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers)
-        ys[rr] = epi.on_row(a + rr, stencil_row<T, false>(S, x, a + rr));
+      const long long off[5] = {-nx, -1, 0, 1, nx};
+      stencil_loop(R0, R1, epi, es, [&](long long r) {
+        return stencil_row_padded<T, 5, false>(S.vals + r, ld, x + r, off, hdiv);
+      });
     }
-    consumer_sync();
-    epi.on_tile(a, nrows, ys);
+  } else if (scaled) {
+    stencil_loop(R0, R1, epi, es, [&](long long r) { return stencil_row<T, true>(S, x, r, hdiv); });
+  } else {
+    stencil_loop(R0, R1, epi, es, [&](long long r) { return stencil_row<T, false>(S, x, r); });
   }
-  epi.on_end();
 }
 
 template <typename T, typename E>

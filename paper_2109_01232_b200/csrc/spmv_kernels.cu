@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, lon
     const int e = rp[r + 1];
     int ok = 1;
     for (int sl = 0; sl < S; ++sl) {
-      T val = T(0);
+      T val = absent_value<T>();   // sentinel for neighbours outside the grid
       if (pres[sl]) {
         if (p < e && (long long)ci[p] == rg + off[sl]) val = v[p++];
         else ok = 0;

@@ -219,12 +219,24 @@ class NativeSolve:
         outer = FP64 if mode == _lib.MODE_IR else prec
         self.outer = outer
         self.ldv = padded_length(n)
-        self.A, self.A64, self.b, self.x = A, A64, b, x
+        if storage not in ("auto", "csr", "stencil"):
+            raise ValueError("storage must be 'auto', 'csr' or 'stencil'")
+        shape = A.stencil_shape() if storage != "csr" else None
+        if shape is None and storage == "stencil":
+            raise ValueError("the matrix is not a 5/7-point Dirichlet stencil")
+        # stencil storage: every SpMV input gets one zeroed grid plane of guard
+        # rows on each side, so the kernel loads all neighbours unconditionally
+        # (absent ones are marked in the packed values, spmv.cuh stencil_row_padded)
+        self.guard = 0 if shape is None else padded_length(shape[1] ** (shape[0] - 1))
+        self.A, self.A64, self.b = A, A64, b
+        self.x = self._guarded(1, outer)
+        self.x.copy_(x[: self.ldv])
         self.r = dvec(n, outer)
         self.r_in = dvec(n, FP32) if mode == _lib.MODE_IR else None
-        self.V = torch.zeros((m + 1) * self.ldv, dtype=prec.torch_dtype, device=device())
+        self.V = self._guarded(m + 1, prec)
         self.w = dvec(n, prec)
-        self.u = dvec(n, prec)
+        self.u = self._guarded(1, prec)
+        x = self.x
         self.state = DeviceState(m, prec)
         self.ws = torch.zeros(int(_lib.load().mpg_workspace_bytes()), dtype=torch.uint8,
                               device=device())
@@ -241,7 +253,7 @@ class NativeSolve:
         self._keep = []
         if pc is not None:
             d.pc_kind, d.pc_prec, d.pc_block = pc.kind, pc.prec.code, pc.block
-            temps = [dvec(n, pc.prec) for _ in range(5)]
+            temps = [self._guarded(1, pc.prec) for _ in range(5)]
             self._keep += temps
             d.pc_t0, d.pc_t1, d.pc_t2, d.pc_t3, d.pc_t4 = (ptr(t) for t in temps)
             if pc.kind == _lib.PC_JACOBI:
@@ -256,31 +268,31 @@ class NativeSolve:
         # stencil-specialised storage: every SpMV of the cycle (Arnoldi operator,
         # polynomial steps, explicit residual) reads packed values instead of CSR
         self.storage = "csr"
-        if storage not in ("auto", "csr", "stencil"):
-            raise ValueError("storage must be 'auto', 'csr' or 'stencil'")
-        if storage != "csr":
-            shape = A.stencil_shape()
-            if shape is None and storage == "stencil":
-                raise ValueError("the matrix is not a 5/7-point Dirichlet stencil")
-            if shape is not None:
-                dia = A.dia()
-                dia64 = A64.dia() if A64 is not None else None
-                pc_dia = None
-                if pc is not None and pc.kind == _lib.PC_POLY:
-                    pcm = A.with_values(pc.values)
-                    pc_dia = pcm.dia()
-                if dia is not None and (A64 is None or dia64 is not None) and \
-                        (pc is None or pc.kind != _lib.PC_POLY or pc_dia is not None):
-                    d.stencil_dims, d.stencil_nx = shape
-                    d.dia = ptr(dia)
-                    d.dia64 = ptr(dia64) if dia64 is not None else None
-                    d.pc_dia = ptr(pc_dia) if pc_dia is not None else None
-                    self._keep += [t for t in (dia, dia64, pc_dia) if t is not None]
-                    self.storage = "stencil"
+        if shape is not None:
+            dia = A.dia()
+            dia64 = A64.dia() if A64 is not None else None
+            pc_dia = None
+            if pc is not None and pc.kind == _lib.PC_POLY:
+                pc_dia = A.with_values(pc.values).dia()
+            if dia is not None and (A64 is None or dia64 is not None) and \
+                    (pc is None or pc.kind != _lib.PC_POLY or pc_dia is not None):
+                d.stencil_dims, d.stencil_nx = shape
+                d.dia = ptr(dia)
+                d.dia64 = ptr(dia64) if dia64 is not None else None
+                d.pc_dia = ptr(pc_dia) if pc_dia is not None else None
+                d.halo = self.guard
+                self._keep += [t for t in (dia, dia64, pc_dia) if t is not None]
+                self.storage = "stencil"
         self.desc = d
         h = C.c_void_p()
         _lib.call("mpg_solver_create", C.byref(d), C.byref(h))
         self.handle = h
+
+    def _guarded(self, rows: int, prec: Precision) -> torch.Tensor:
+        """`rows` zeroed vectors of stride ldv with `guard` readable rows on each side."""
+        g = self.guard
+        buf = torch.zeros(rows * self.ldv + 2 * g, dtype=prec.torch_dtype, device=device())
+        return buf[g: g + rows * self.ldv]
 
     def close(self) -> None:
         if self.handle:
@@ -416,7 +428,7 @@ def gmres_restarted(A, b, x0=None, criteria: StopCriteria | None = None, precond
     finally:
         ns.close()
     fp32 = precision is FP32
-    x = xd[:n]
+    x = ns.x[:n]
     if fp32:
         x = convert_vector(x, FP64)
     return SolveReport(
@@ -488,7 +500,7 @@ def gmres_ir(A, b, x0=None, criteria: StopCriteria | None = None, precond_fp32=N
     finally:
         ns.close()
     return SolveReport(
-        x=_out(xd, n, host), converged=converged, total_iters=total, iters_fp32=total,
+        x=_out(ns.x, n, host), converged=converged, total_iters=total, iters_fp32=total,
         iters_fp64=0, residual_history=history, kernel_times=timer.breakdown(),
         loss_of_accuracy=False, stalled_at=stalled_at, total_time=timer.total)
 
@@ -523,7 +535,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
                 _, iters32, loss32, stalled_at = _run_restarted(
                     ns32, criteria, "fp32", history, iter_offset=0,
                     limit=min(switch_iter, criteria.max_iters), stop_on_stall=True)
-                xd = padded_copy(convert_vector(x32[:n], FP64), FP64)
+                xd = padded_copy(convert_vector(ns32.x[:n], FP64), FP64)
         finally:
             ns32.close()
         if history and history[-1].iteration == iters32:
@@ -538,7 +550,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
     finally:
         ns.close()
     return SolveReport(
-        x=_out(xd, n, host), converged=converged, total_iters=iters32 + iters64,
+        x=_out(ns.x, n, host), converged=converged, total_iters=iters32 + iters64,
         iters_fp32=iters32, iters_fp64=iters64, residual_history=history,
         kernel_times=timer.breakdown(), loss_of_accuracy=loss32 or loss64,
         stalled_at=stalled_at if stalled_at is not None else st64, total_time=timer.total)
