@@ -332,7 +332,11 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
   if (gated(sv.h)) return;
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
-  __shared__ __align__(16) T upart[2][kWarps][RB];
+  constexpr int RPW = RB / kWarps;   // rows each warp reduces per block
+  // single-buffered: a warp writes upart (xs) of block it+1 only after the
+  // barrier every warp reaches once done reading upart (xs) of block it
+  __shared__ __align__(16) T upart[kWarps][RB];
+  __shared__ __align__(16) T xs[RB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   T c1q[KV], acc[KV];
 #pragma unroll
@@ -358,17 +362,10 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
         for (int e = 0; e < VN; ++e) v[q][e] = (i < k && r + e < R1) ? __ldcs(V + (size_t)i * ldv + r + e) : T(0);
       }
     }
-    // every warp reads this block of w before the barrier; warp 0 overwrites
-    // it only after the barrier, so no warp can observe the updated values
-    T wv[VN];
-    if (full) {
-      const auto q4 = *reinterpret_cast<const typename Vec<T>::type*>(w + r);
-      if constexpr (VN == 4) { wv[0] = q4.x; wv[1] = q4.y; wv[2] = q4.z; wv[3] = q4.w; }
-      else { wv[0] = q4.x; wv[1] = q4.y; }
-    } else {
-#pragma unroll
-      for (int e = 0; e < VN; ++e) wv[e] = (r + e < R1) ? w[r + e] : T(0);
-    }
+    // reducer lane: row rb + rrow of this block (warp w owns RPW rows of it)
+    const int rrow = warp * RPW + lane;
+    const bool reducer = lane < RPW && rb + rrow < R1;
+    const T wv = reducer ? w[rb + rrow] : T(0);
     T u[VN];
 #pragma unroll
     for (int e = 0; e < VN; ++e) u[e] = T(0);
@@ -376,31 +373,22 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
     for (int q = 0; q < KV; ++q)
 #pragma unroll
       for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c1q[q], u[e]);
-    T* up = upart[it & 1][warp] + lane * VN;
-#pragma unroll
-    for (int e = 0; e < VN; ++e) up[e] = u[e];
+    vstore(upart[warp] + lane * VN, u);
     __syncthreads();
-    T s[VN], x[VN];
+    // the 8 warp partials of each row are summed in warp order by one lane
+    if (reducer) {
+      T s = T(0);
 #pragma unroll
-    for (int e = 0; e < VN; ++e) s[e] = T(0);
-#pragma unroll
-    for (int ww = 0; ww < kWarps; ++ww) {
-      T t[VN];
-      vload_smem(upart[it & 1][ww] + lane * VN, t);
-#pragma unroll
-      for (int e = 0; e < VN; ++e) s[e] += t[e];
+      for (int ww = 0; ww < kWarps; ++ww) s += upart[ww][rrow];
+      const T xr = sub_rn(wv, s);
+      xs[rrow] = xr;
+      w[rb + rrow] = xr;
+    } else if (lane < RPW) {
+      xs[rrow] = T(0);
     }
-#pragma unroll
-    for (int e = 0; e < VN; ++e) x[e] = (r + e < R1) ? sub_rn(wv[e], s[e]) : T(0);
-    if (warp == 0) {
-      if (full) {
-        vstore(w + r, x);
-      } else {
-#pragma unroll
-        for (int e = 0; e < VN; ++e)
-          if (r + e < R1) w[r + e] = x[e];
-      }
-    }
+    __syncthreads();
+    T x[VN];
+    vload_smem(xs + lane * VN, x);
 #pragma unroll
     for (int q = 0; q < KV; ++q)
 #pragma unroll
