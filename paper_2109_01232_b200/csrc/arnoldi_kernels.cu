@@ -333,10 +333,12 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
   constexpr int RPW = RB / kWarps;   // rows each warp reduces per block
-  // single-buffered: a warp writes upart (xs) of block it+1 only after the
-  // barrier every warp reaches once done reading upart (xs) of block it
-  __shared__ __align__(16) T upart[kWarps][RB];
-  __shared__ __align__(16) T xs[RB];
+  // U blocks per barrier pair: more loads in flight for small KV
+  constexpr int U = KV <= 2 ? 4 : (KV <= 4 ? 2 : 1);
+  // single-buffered: a warp writes upart (xs) of group it+1 only after the
+  // barrier every warp reaches once done reading upart (xs) of group it
+  __shared__ __align__(16) T upart[U][kWarps][RB];
+  __shared__ __align__(16) T xs[U][RB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   T c1q[KV], acc[KV];
 #pragma unroll
@@ -347,52 +349,70 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
   }
   long long R0, R1;
   cta_rows(n, R0, R1);
-  int it = 0;
-  for (long long rb = R0; rb < R1; rb += RB, ++it) {
-    const long long r = rb + (long long)lane * VN;
-    const bool full = r + VN <= R1;
-    T v[KV][VN];
+  for (long long rg = R0; rg < R1; rg += (long long)U * RB) {
+    T v[U][KV][VN];
 #pragma unroll
-    for (int q = 0; q < KV; ++q) {
-      const int i = warp + kWarps * q;
-      if (i < k && full) {
-        vload_cs(V + (size_t)i * ldv + r, v[q]);
-      } else {
+    for (int b = 0; b < U; ++b) {
+      const long long r = rg + (long long)b * RB + (long long)lane * VN;
+      const bool full = r + VN <= R1;
 #pragma unroll
-        for (int e = 0; e < VN; ++e) v[q][e] = (i < k && r + e < R1) ? __ldcs(V + (size_t)i * ldv + r + e) : T(0);
+      for (int q = 0; q < KV; ++q) {
+        const int i = warp + kWarps * q;
+        if (i < k && full) {
+          vload_cs(V + (size_t)i * ldv + r, v[b][q]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VN; ++e)
+            v[b][q][e] = (i < k && r + e < R1) ? __ldcs(V + (size_t)i * ldv + r + e) : T(0);
+        }
       }
     }
-    // reducer lane: row rb + rrow of this block (warp w owns RPW rows of it)
+    // reducer lane: row rrow of each block (warp w owns RPW rows of it)
     const int rrow = warp * RPW + lane;
-    const bool reducer = lane < RPW && rb + rrow < R1;
-    const T wv = reducer ? w[rb + rrow] : T(0);
-    T u[VN];
+    T wv[U];
 #pragma unroll
-    for (int e = 0; e < VN; ++e) u[e] = T(0);
+    for (int b = 0; b < U; ++b) {
+      const long long rr = rg + (long long)b * RB + rrow;
+      wv[b] = (lane < RPW && rr < R1) ? w[rr] : T(0);
+    }
 #pragma unroll
-    for (int q = 0; q < KV; ++q)
+    for (int b = 0; b < U; ++b) {
+      T u[VN];
 #pragma unroll
-      for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c1q[q], u[e]);
-    vstore(upart[warp] + lane * VN, u);
-    __syncthreads();
-    // the 8 warp partials of each row are summed in warp order by one lane
-    if (reducer) {
-      T s = T(0);
+      for (int e = 0; e < VN; ++e) u[e] = T(0);
 #pragma unroll
-      for (int ww = 0; ww < kWarps; ++ww) s += upart[ww][rrow];
-      const T xr = sub_rn(wv, s);
-      xs[rrow] = xr;
-      w[rb + rrow] = xr;
-    } else if (lane < RPW) {
-      xs[rrow] = T(0);
+      for (int q = 0; q < KV; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[b][q][e], c1q[q], u[e]);
+      vstore(upart[b][warp] + lane * VN, u);
     }
     __syncthreads();
-    T x[VN];
-    vload_smem(xs + lane * VN, x);
+    // the 8 warp partials of each row are summed in warp order by one lane
+    if (lane < RPW) {
 #pragma unroll
-    for (int q = 0; q < KV; ++q)
+      for (int b = 0; b < U; ++b) {
+        const long long rr = rg + (long long)b * RB + rrow;
+        T xr = T(0);
+        if (rr < R1) {
+          T s = T(0);
 #pragma unroll
-      for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], x[e], acc[q]);
+          for (int ww = 0; ww < kWarps; ++ww) s += upart[b][ww][rrow];
+          xr = sub_rn(wv[b], s);
+          w[rr] = xr;
+        }
+        xs[b][rrow] = xr;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < U; ++b) {
+      T x[VN];
+      vload_smem(xs[b] + lane * VN, x);
+#pragma unroll
+      for (int q = 0; q < KV; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[b][q][e], x[e], acc[q]);
+    }
   }
   T* part = static_cast<T*>(ws.part);
 #pragma unroll
