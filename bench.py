@@ -191,6 +191,10 @@ def native_arm(args, rank: int, world: int):
         used = ns.storage
         ns.close()
         model = cycle_bytes(n, nnz, M, 4, used)
+        if prof.get("scale", (0.0, 0))[1] == 0:
+            # K_S fused into K_C (k_update_norm_scale): read V + w', write v = (k+2) n s,
+            # the same count as update_norm_givens; no separate scale traffic
+            model.pop("scale")
         kernels = {}
         for k, (ms, cnt) in prof.items():
             kernels[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}

@@ -9,6 +9,7 @@
 // so the basis is swept three times per step (the reference's BLAS sequence
 // sweeps it four times).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "spmv.cuh"
@@ -667,6 +668,130 @@ __global__ void __launch_bounds__(kThreads) k_step_scale(const T* __restrict__ w
     vn[r] = div_rn(w[r], hs);
 }
 
+// ============================================ K_CS update_norm + scale, fused
+// K_C and K_S in one cooperative launch (every CTA co-resident):
+//   phase 1  w' = w - V c2 for the CTA's rows, kept in shared memory (CACHE)
+//            or written back (L2-resident re-read); per-CTA ||w'||^2 partial
+//   barrier  one grid-wide barrier
+//   phase 2  every CTA sums the partials in the same fixed order as k_update_norm's
+//            last CTA (bitwise the same h_sub), CTA 0 does the Givens rotation, and
+//            every CTA writes V[:, j+1] = w' / h_sub for its rows (krylov.py:148)
+// This drops K_S's launch and its 2 n s bytes (read w, write v) for n s (write v).
+// Shared arrival counter + generation word in the workspace; the last arriver
+// resets the counter before releasing, so the slot is reusable.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g0 = ld_acquire_u32(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      atomicExch(count, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire_u32(gen) == g0) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename T, bool CACHE>
+__global__ void __launch_bounds__(kThreads) k_update_norm_scale(const T* __restrict__ V, long long ldv,
+                                                                long long n, int j, T* __restrict__ w,
+                                                                StateView<T> sv, WsView ws, int m_limit,
+                                                                int kpad) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  const int k = j + 1;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  T* c2s = reinterpret_cast<T*>(smraw);
+  T* wsm = c2s + kpad;   // CACHE: this CTA's rows of w'
+  __shared__ T red[32];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) c2s[i] = sv.c2[i];
+  __syncthreads();
+  long long R0, R1;
+  cta_rows(n, R0, R1);
+  T ss = T(0);
+  const long long nv = (R1 - R0) / VN;
+  for (long long g = threadIdx.x; g < nv; g += kThreads) {
+    const long long r = R0 + g * VN;
+    T wv[VN], u[VN];
+    vload(w + r, wv);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) u[e] = T(0);
+    int i = 0;
+    for (; i + 4 <= k; i += 4) {
+      T v0[VN], v1[VN], v2[VN], v3[VN];
+      vload_cs(V + (size_t)(i + 0) * ldv + r, v0);
+      vload_cs(V + (size_t)(i + 1) * ldv + r, v1);
+      vload_cs(V + (size_t)(i + 2) * ldv + r, v2);
+      vload_cs(V + (size_t)(i + 3) * ldv + r, v3);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        u[e] = fma_rn(v0[e], c2s[i + 0], u[e]);
+        u[e] = fma_rn(v1[e], c2s[i + 1], u[e]);
+        u[e] = fma_rn(v2[e], c2s[i + 2], u[e]);
+        u[e] = fma_rn(v3[e], c2s[i + 3], u[e]);
+      }
+    }
+    for (; i < k; ++i) {
+      T v0[VN];
+      vload_cs(V + (size_t)i * ldv + r, v0);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) u[e] = fma_rn(v0[e], c2s[i], u[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      wv[e] = sub_rn(wv[e], u[e]);
+      ss = fma_rn(wv[e], wv[e], ss);
+    }
+    if (CACHE) vstore(wsm + g * VN, wv);
+    else vstore(w + r, wv);
+  }
+  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads) {
+    T u = T(0);
+    for (int i = 0; i < k; ++i) u = fma_rn(__ldcs(V + (size_t)i * ldv + r), c2s[i], u);
+    const T wv = sub_rn(w[r], u);
+    if (CACHE) wsm[r - R0] = wv;
+    else w[r] = wv;
+    ss = fma_rn(wv, wv, ss);
+  }
+  const T t = block_sum(ss, red);
+  T* part = static_cast<T*>(ws.part);
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+  grid_barrier(ws.counter, ws.counter + 1);
+  // the same fixed-order sum in every CTA (identical to k_update_norm's last CTA)
+  T s = T(0);
+  for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
+  s = block_sum(s, red);
+  const T hs = sqrt_rn(s);
+  const bool brk = (double)hs <= sv.h->breakdown_tol * sv.h->w0;   // krylov.py:146
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    sv.Hc(j, j + 1) = hs;
+    sv.h->h_sub = (double)hs;
+    givens_column(sv, j, sv.h->threshold, brk, m_limit);
+  }
+  if (brk) return;   // no new basis vector on breakdown
+  T* vn = const_cast<T*>(V) + (size_t)(j + 1) * ldv;
+  for (long long g = threadIdx.x; g < nv; g += kThreads) {
+    const long long r = R0 + g * VN;
+    T a[VN];
+    if (CACHE) vload_smem(wsm + g * VN, a);
+    else vload(w + r, a);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);
+    vstore(vn + r, a);
+  }
+  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads)
+    vn[r] = div_rn(CACHE ? wsm[r - R0] : w[r], hs);
+}
+
 // ===================================================================== start
 
 // Reset the cycle state (krylov.py:62-68, 96-100) — whole CTA.
@@ -973,6 +1098,16 @@ __global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, l
 
 // ================================================================= launchers
 
+// MPG_FUSE_CS=0 selects the separate K_C + K_S launches (A/B measurement)
+bool fuse_update_norm_scale() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_FUSE_CS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int g_sms = 0;
 int num_sms() {
   if (!g_sms) {
@@ -1167,6 +1302,81 @@ cudaError_t launch_update_norm(const T* V, long long ldv, long long n, int j, T*
   return cudaGetLastError();
 }
 
+// K_CS grid: the largest co-resident grid (<= 6 CTAs/SM, K_C's occupancy) for
+// which the CTA's row slice of w' fits in shared memory; else the uncached
+// variant at full occupancy.  Returns 0 when no cooperative grid is possible.
+template <typename T>
+struct UnsPlan { unsigned grid = 0; size_t smem = 0; bool cache = false; };
+
+template <typename T>
+static UnsPlan<T> plan_update_norm_scale(long long n, int m) {
+  static std::once_flag once;
+  static int dev_smem_optin = 0;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&dev_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_update_norm_scale<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         dev_smem_optin - 1024);
+    cudaFuncSetAttribute(k_update_norm_scale<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (kMaxM + 16) * (int)sizeof(T));
+    cudaGetLastError();
+  });
+  UnsPlan<T> p;
+  constexpr int VN = Vec<T>::n;
+  const int kpad = (m + 16) & ~7;
+  const size_t base = (size_t)kpad * sizeof(T);
+  long long tiles = (n + (long long)kThreads * VN - 1) / ((long long)kThreads * VN);
+  if (tiles < 1) tiles = 1;
+  for (int occ = 6; occ >= 1; --occ) {
+    long long G = std::min<long long>((long long)num_sms() * occ, tiles);
+    // cta_rows: each CTA's slice is at most ceil(n / G) + kRowAlign rows
+    const long long rows = (n + G - 1) / G + kRowAlign;
+    const size_t smem = base + (size_t)rows * sizeof(T);
+    if (smem > (size_t)(dev_smem_optin - 1024)) continue;
+    int got = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, k_update_norm_scale<T, true>, kThreads, smem) !=
+        cudaSuccess) { cudaGetLastError(); continue; }
+    if ((long long)got * num_sms() >= G) { p.grid = (unsigned)G; p.smem = smem; p.cache = true; return p; }
+  }
+  int got = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&got, k_update_norm_scale<T, false>, kThreads, base) ==
+          cudaSuccess && got >= 1) {
+    p.grid = (unsigned)std::min<long long>((long long)num_sms() * std::min(got, 6), tiles);
+    p.smem = base;
+    p.cache = false;
+  }
+  cudaGetLastError();
+  return p;
+}
+
+template <typename T>
+cudaError_t launch_update_norm_scale(const T* V, long long ldv, long long n, int j, T* w,
+                                     StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+  if (j + 1 > sv.m) return cudaErrorInvalidValue;
+  const UnsPlan<T> p = plan_update_norm_scale<T>(n, sv.m);
+  if (!p.grid) {   // no co-resident grid: separate K_C + K_S
+    const cudaError_t e = launch_update_norm<T>(V, ldv, n, j, w, sv, ws, m_limit, st);
+    if (e != cudaSuccess) return e;
+    return launch_step_scale<T>(w, const_cast<T*>(V) + (size_t)(j + 1) * ldv, n, j, sv, st);
+  }
+  const int kpad = (sv.m + 16) & ~7;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  if (p.cache)
+    return cudaLaunchKernelEx(&cfg, k_update_norm_scale<T, true>, V, ldv, n, j, w, sv, ws, m_limit, kpad);
+  return cudaLaunchKernelEx(&cfg, k_update_norm_scale<T, false>, V, ldv, n, j, w, sv, ws, m_limit, kpad);
+}
+
 template <typename T>
 cudaError_t launch_step_scale(const T* w, T* vnext, long long n, int j, StateView<T> sv,
                               cudaStream_t st) {
@@ -1253,6 +1463,8 @@ cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> 
                                              StateView<T>, WsView, int, cudaStream_t);         \
   template cudaError_t launch_step_scale<T>(const T*, T*, long long, int, StateView<T>,         \
                                             cudaStream_t);                                     \
+  template cudaError_t launch_update_norm_scale<T>(const T*, long long, long long, int, T*,     \
+                                                   StateView<T>, WsView, int, cudaStream_t);   \
   template cudaError_t launch_start<T>(const T*, long long, StateView<T>, double, const double*, \
                                        double, WsView, cudaStream_t);                          \
   template cudaError_t launch_start_scale<T>(const T*, T*, long long, StateView<T>,             \

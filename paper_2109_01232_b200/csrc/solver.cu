@@ -255,6 +255,11 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       }));
     }
     { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, wj, sv, ws, st)); }
+    if (fuse_update_norm_scale() && !fuse) {
+      ProfScope ps(PK_UPDATE_NORM);
+      TRY(launch_update_norm_scale<T>(V, d.ldv, d.n, j, wj, sv, ws, m_limit, st));
+      continue;
+    }
     { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, wj, sv, ws, m_limit, st)); }
     if (!fuse) {
       ProfScope ps(PK_SCALE);

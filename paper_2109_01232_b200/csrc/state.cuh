@@ -119,6 +119,11 @@ cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* 
 template <typename T>
 cudaError_t launch_update_norm(const T* V, long long ldv, long long n, int j, T* w,
                                StateView<T> sv, WsView ws, int m_limit, cudaStream_t st);
+// K_C + K_S in one cooperative launch (grid barrier); falls back to the pair
+template <typename T>
+cudaError_t launch_update_norm_scale(const T* V, long long ldv, long long n, int j, T* w,
+                                     StateView<T> sv, WsView ws, int m_limit, cudaStream_t st);
+bool fuse_update_norm_scale();
 template <typename T>
 cudaError_t launch_step_scale(const T* w, T* vnext, long long n, int j, StateView<T> sv,
                               cudaStream_t st);

@@ -4,6 +4,7 @@ Run in the build container, where the read-only reference exists:
 
     python tests/golden/make_golden.py            # small + assembly hashes
     python tests/golden/make_golden.py --cfg2     # + full Laplace3D(150) runs (~35 min)
+    python tests/golden/make_golden.py --skip-small --cfg3   # ConvDiff2D(1500) runs (~28 min)
 
 Nothing on the GPU box reads /root/reference: the tests only read the
 committed JSON/NPZ written here.  The reference is imported read-only from
@@ -88,6 +89,12 @@ CFG2_RUNS = [
     ("laplace3d:150/ir/m50", ("laplace3d", 150, {}), "ir", {"m": 50}),
 ]
 
+CFG3_RUNS = [  # BASELINE configs[2]: UniFlow2D 1500^2 (convection=1501, dx_term 0.5)
+    ("convdiff2d:1500:c1501/fp64/m50", ("convdiff2d", 1500, {"convection": 1501.0}), "fp64", {"m": 50}),
+    ("convdiff2d:1500:c1501/ir+jacobi1/m50", ("convdiff2d", 1500, {"convection": 1501.0}), "ir+jacobi1",
+     {"m": 50}),
+]
+
 
 def run_one(mp, spec, solver, kw):
     kind, nx, sk = spec
@@ -158,6 +165,7 @@ def spmv_fixtures(mp):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--cfg3", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
     mp = _ref()
@@ -189,6 +197,14 @@ def main():
             runs[name] = report_dict(run_one(mp, spec, solver, kw))
             print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg2.json"), "w") as f:
+            json.dump({"meta": meta, "runs": runs}, f, indent=1)
+    if args.cfg3:
+        runs = {}
+        for name, spec, solver, kw in CFG3_RUNS:
+            t = time.time()
+            runs[name] = report_dict(run_one(mp, spec, solver, kw))
+            print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
+        with open(os.path.join(HERE, "reference_cfg3.json"), "w") as f:
             json.dump({"meta": meta, "runs": runs}, f, indent=1)
 
 
