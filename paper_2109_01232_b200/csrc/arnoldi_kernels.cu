@@ -348,9 +348,9 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
     c1q[q] = i < k ? sv.c1[i] : T(0);
     acc[q] = T(0);
   }
-  long long R0, R1;
-  cta_rows(n, R0, R1);
-  for (long long rg = R0; rg < R1; rg += (long long)U * RB) {
+  // grid-stride over blocks of U * RB rows (one compact window of V streams at a time)
+  const long long R1 = n;
+  for (long long rg = (long long)blockIdx.x * U * RB; rg < R1; rg += (long long)gridDim.x * U * RB) {
     T v[U][KV][VN];
 #pragma unroll
     for (int b = 0; b < U; ++b) {
@@ -583,12 +583,13 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ 
   __shared__ T red[32];
   for (int i = threadIdx.x; i < k; i += blockDim.x) c2s[i] = sv.c2[i];
   __syncthreads();
-  long long R0, R1;
-  cta_rows(n, R0, R1);
+  // grid-stride 16-byte row groups, the same order as k_update_norm_scale (launched
+  // on the same grid, so the distributed phases are bitwise the fused kernel)
+  const long long ng = (n + VN - 1) / VN;
+  const long long stride = (long long)gridDim.x * kThreads;
   T ss = T(0);
-  const long long nv = (R1 - R0) / VN;
-  for (long long g = threadIdx.x; g < nv; g += kThreads) {
-    const long long r = R0 + g * VN;
+  for (long long g = blockIdx.x * (long long)kThreads + threadIdx.x; g < ng; g += stride) {
+    const long long r = g * VN;
     T wv[VN], u[VN];
     vload(w + r, wv);
 #pragma unroll
@@ -616,17 +617,10 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ 
     }
 #pragma unroll
     for (int e = 0; e < VN; ++e) {
-      wv[e] = sub_rn(wv[e], u[e]);
+      wv[e] = r + e < n ? sub_rn(wv[e], u[e]) : T(0);
       ss = fma_rn(wv[e], wv[e], ss);
     }
     vstore(w + r, wv);
-  }
-  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads) {
-    T u = T(0);
-    for (int i = 0; i < k; ++i) u = fma_rn(__ldcs(V + (size_t)i * ldv + r), c2s[i], u);
-    const T wv = sub_rn(w[r], u);
-    w[r] = wv;
-    ss = fma_rn(wv, wv, ss);
   }
   const T t = block_sum(ss, red);
   T* part = static_cast<T*>(ws.part);
@@ -711,16 +705,19 @@ __global__ void __launch_bounds__(kThreads) k_update_norm_scale(const T* __restr
   const int k = j + 1;
   extern __shared__ __align__(128) unsigned char smraw[];
   T* c2s = reinterpret_cast<T*>(smraw);
-  T* wsm = c2s + kpad;   // CACHE: this CTA's rows of w'
+  T* wsm = c2s + kpad;   // CACHE: this CTA's groups of w', slot it * kThreads + tid
   __shared__ T red[32];
   for (int i = threadIdx.x; i < k; i += blockDim.x) c2s[i] = sv.c2[i];
   __syncthreads();
-  long long R0, R1;
-  cta_rows(n, R0, R1);
+  // grid-stride over 16-byte row groups: at any moment the whole grid streams one
+  // compact window of every basis vector (measured faster than per-CTA slices);
+  // rows in [n, ldv) are zero padding and are masked out of w'
+  const long long ng = (n + VN - 1) / VN;
+  const long long stride = (long long)gridDim.x * kThreads;
   T ss = T(0);
-  const long long nv = (R1 - R0) / VN;
-  for (long long g = threadIdx.x; g < nv; g += kThreads) {
-    const long long r = R0 + g * VN;
+  int it = 0;
+  for (long long g = blockIdx.x * (long long)kThreads + threadIdx.x; g < ng; g += stride, ++it) {
+    const long long r = g * VN;
     T wv[VN], u[VN];
     vload(w + r, wv);
 #pragma unroll
@@ -748,19 +745,11 @@ __global__ void __launch_bounds__(kThreads) k_update_norm_scale(const T* __restr
     }
 #pragma unroll
     for (int e = 0; e < VN; ++e) {
-      wv[e] = sub_rn(wv[e], u[e]);
+      wv[e] = r + e < n ? sub_rn(wv[e], u[e]) : T(0);
       ss = fma_rn(wv[e], wv[e], ss);
     }
-    if (CACHE) vstore(wsm + g * VN, wv);
+    if (CACHE) vstore(wsm + ((size_t)it * kThreads + threadIdx.x) * VN, wv);
     else vstore(w + r, wv);
-  }
-  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads) {
-    T u = T(0);
-    for (int i = 0; i < k; ++i) u = fma_rn(__ldcs(V + (size_t)i * ldv + r), c2s[i], u);
-    const T wv = sub_rn(w[r], u);
-    if (CACHE) wsm[r - R0] = wv;
-    else w[r] = wv;
-    ss = fma_rn(wv, wv, ss);
   }
   const T t = block_sum(ss, red);
   T* part = static_cast<T*>(ws.part);
@@ -779,17 +768,15 @@ __global__ void __launch_bounds__(kThreads) k_update_norm_scale(const T* __restr
   }
   if (brk) return;   // no new basis vector on breakdown
   T* vn = const_cast<T*>(V) + (size_t)(j + 1) * ldv;
-  for (long long g = threadIdx.x; g < nv; g += kThreads) {
-    const long long r = R0 + g * VN;
+  it = 0;
+  for (long long g = blockIdx.x * (long long)kThreads + threadIdx.x; g < ng; g += stride, ++it) {
     T a[VN];
-    if (CACHE) vload_smem(wsm + g * VN, a);
-    else vload(w + r, a);
+    if (CACHE) vload_smem(wsm + ((size_t)it * kThreads + threadIdx.x) * VN, a);
+    else vload_cg(w + g * VN, a);   // written by this thread in this launch: L2 path
 #pragma unroll
-    for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);
-    vstore(vn + r, a);
+    for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);   // padding stays 0
+    vstore(vn + g * VN, a);
   }
-  for (long long r = R0 + nv * VN + threadIdx.x; r < R1; r += kThreads)
-    vn[r] = div_rn(CACHE ? wsm[r - R0] : w[r], hs);
 }
 
 // ===================================================================== start
@@ -1283,25 +1270,6 @@ cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k,
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_update_norm(const T* V, long long ldv, long long n, int j, T* w,
-                               StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(k_update_norm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (kMaxM + 8) * (int)sizeof(T));
-  });
-  constexpr int VN = Vec<T>::n;
-  long long G = (n + (long long)kThreads * VN - 1) / ((long long)kThreads * VN);
-  const long long cap = (long long)num_sms() * 6;
-  if (G > cap) G = cap;
-  if (G < 1) G = 1;
-  count_launch();
-  k_update_norm<T><<<(unsigned)G, kThreads, (size_t)(j + 9) * sizeof(T), st>>>(V, ldv, n, j, w, sv, ws,
-                                                                                 m_limit);
-  return cudaGetLastError();
-}
-
 // K_CS grid: the largest co-resident grid (<= 6 CTAs/SM, K_C's occupancy) for
 // which the CTA's row slice of w' fits in shared memory; else the uncached
 // variant at full occupancy.  Returns 0 when no cooperative grid is possible.
@@ -1330,8 +1298,9 @@ static UnsPlan<T> plan_update_norm_scale(long long n, int m) {
   if (tiles < 1) tiles = 1;
   for (int occ = 6; occ >= 1; --occ) {
     long long G = std::min<long long>((long long)num_sms() * occ, tiles);
-    // cta_rows: each CTA's slice is at most ceil(n / G) + kRowAlign rows
-    const long long rows = (n + G - 1) / G + kRowAlign;
+    // grid-stride groups: each CTA caches ceil(groups / (G * kThreads)) * kThreads groups
+    const long long groups = (n + VN - 1) / VN;
+    const long long rows = (groups + G * kThreads - 1) / (G * kThreads) * kThreads * VN;
     const size_t smem = base + (size_t)rows * sizeof(T);
     if (smem > (size_t)(dev_smem_optin - 1024)) continue;
     int got = 0;
@@ -1348,6 +1317,28 @@ static UnsPlan<T> plan_update_norm_scale(long long n, int m) {
   }
   cudaGetLastError();
   return p;
+}
+
+template <typename T>
+cudaError_t launch_update_norm(const T* V, long long ldv, long long n, int j, T* w,
+                               StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(k_update_norm<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (kMaxM + 8) * (int)sizeof(T));
+  });
+  constexpr int VN = Vec<T>::n;
+  long long G = (n + (long long)kThreads * VN - 1) / ((long long)kThreads * VN);
+  const long long cap = (long long)num_sms() * 6;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  // the fused K_CS grid when there is one: identical partials and norm
+  const unsigned pg = plan_update_norm_scale<T>(n, sv.m).grid;
+  if (pg) G = pg;
+  count_launch();
+  k_update_norm<T><<<(unsigned)G, kThreads, (size_t)(j + 9) * sizeof(T), st>>>(V, ldv, n, j, w, sv, ws,
+                                                                                 m_limit);
+  return cudaGetLastError();
 }
 
 template <typename T>

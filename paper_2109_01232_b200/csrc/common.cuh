@@ -57,6 +57,13 @@ __device__ __forceinline__ void vload_cs(const T* p, T (&v)[Vec<T>::n]) {
   if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
   else { v[0] = q.x; v[1] = q.y; }
 }
+// L2 (coherent) load: for data written earlier in the same launch
+template <typename T>
+__device__ __forceinline__ void vload_cg(const T* p, T (&v)[Vec<T>::n]) {
+  auto q = __ldcg(reinterpret_cast<const typename Vec<T>::type*>(p));
+  if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
+  else { v[0] = q.x; v[1] = q.y; }
+}
 template <typename T>
 __device__ __forceinline__ void vload_smem(const T* p, T (&v)[Vec<T>::n]) {
   auto q = *reinterpret_cast<const typename Vec<T>::type*>(p);

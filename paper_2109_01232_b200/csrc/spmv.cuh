@@ -1,7 +1,7 @@
 // CSR SpMV tile pipeline for sm_100a.
 //
-// Each persistent CTA owns a contiguous, 32-row-aligned slice of rows and
-// walks it in tiles of kSpTile rows.  One producer warp streams each tile's
+// Each persistent CTA walks tiles of kSpTile rows dealt round-robin over the
+// grid (tile = blockIdx.x + i * gridDim.x).  One producer warp streams each tile's
 // row_ptr slice, col_idx range and values range into shared memory with 1-D
 // TMA bulk copies (cp.async.bulk -> UBLKCP) into a 2-stage ring guarded by
 // full/empty mbarriers; eight consumer warps compute one row per thread with
@@ -279,12 +279,17 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
   return stencil_reduce<T, 5>(pr, pv, px);
 }
 
+// Tiles are dealt round-robin (tile = blockIdx.x + i * gridDim.x): the whole grid
+// streams one compact window of the basis at a time, measured faster on B200
+// than contiguous per-CTA slices (tools/bw_probe.cu).
 template <typename T, typename E, typename RowF>
-__device__ __forceinline__ void stencil_loop(long long R0, long long R1, E& epi, EpiShared<T>& es,
+__device__ __forceinline__ void stencil_loop(long long n, E& epi, EpiShared<T>& es,
                                              const RowF& rowf) {
+  const long long ntiles = (n + kSpTile - 1) / kSpTile;
   int t = 0;
-  for (long long a = R0; a < R1; a += kSpTile, ++t) {
-    const int nrows = (int)min((long long)kSpTile, R1 - a);
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+    const long long a = tile * kSpTile;
+    const int nrows = (int)min((long long)kSpTile, n - a);
     T* ys = es.ys[t & 1];
     for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers) ys[rr] = epi.on_row(a + rr, rowf(a + rr));
     consumer_sync();
@@ -296,8 +301,7 @@ __device__ __forceinline__ void stencil_loop(long long R0, long long R1, E& epi,
 template <typename T, typename E>
 __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
                                                  E& epi, EpiShared<T>& es) {
-  long long R0, R1;
-  cta_rows(S.n, R0, R1);
+  const long long n = S.n;
   const bool scaled = S.xdiv != nullptr;
   const T hdiv = scaled ? __ldg(S.xdiv) : T(1);
   const size_t ld = (size_t)S.ldv;
@@ -305,28 +309,30 @@ __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const 
     const long long nx = S.nx, p2 = nx * nx;
     if (S.dims == 3) {
       const long long off[7] = {-p2, -nx, -1, 0, 1, nx, p2};
-      stencil_loop(R0, R1, epi, es, [&](long long r) {
+      stencil_loop(n, epi, es, [&](long long r) {
         return stencil_row_padded<T, 7, false>(S.vals + r, ld, x + r, off, hdiv);
       });
     } else {
       const long long off[5] = {-nx, -1, 0, 1, nx};
-      stencil_loop(R0, R1, epi, es, [&](long long r) {
+      stencil_loop(n, epi, es, [&](long long r) {
         return stencil_row_padded<T, 5, false>(S.vals + r, ld, x + r, off, hdiv);
       });
     }
   } else if (scaled) {
-    stencil_loop(R0, R1, epi, es, [&](long long r) { return stencil_row<T, true>(S, x, r, hdiv); });
+    stencil_loop(n, epi, es, [&](long long r) { return stencil_row<T, true>(S, x, r, hdiv); });
   } else {
-    stencil_loop(R0, R1, epi, es, [&](long long r) { return stencil_row<T, false>(S, x, r); });
+    stencil_loop(n, epi, es, [&](long long r) { return stencil_row<T, false>(S, x, r); });
   }
 }
 
 template <typename T, typename E>
 __device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __restrict__ x,
                                               E& epi, SpSmem<T>& sm) {
-  long long R0, R1;
-  cta_rows(A.n, R0, R1);
-  const int nt = (int)((R1 - R0 + kSpTile - 1) / kSpTile);
+  // round-robin tiles, as stencil_loop: tile t of this CTA starts at row_of(t)
+  const long long ntiles = (A.n + kSpTile - 1) / kSpTile;
+  const int nt = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  auto row_of = [&](int t) { return ((long long)blockIdx.x + (long long)t * gridDim.x) * kSpTile; };
+  const long long R1 = A.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -341,7 +347,7 @@ __device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __re
   if (warp == kSpConsumerWarps) {
     // ------------------------------ producer warp ------------------------------
     if (lane == 0) {
-      long long nb_a = R0, nb_b = (nt > 0) ? min(R0 + kSpTile, R1) : R0;
+      long long nb_a = row_of(0), nb_b = (nt > 0) ? min(nb_a + kSpTile, R1) : nb_a;
       int next_base = (nt > 0) ? __ldg(A.rp + nb_a) : 0;
       int next_end = (nt > 0) ? __ldg(A.rp + nb_b) : 0;
       for (int t = 0; t < nt; ++t) {
@@ -350,9 +356,9 @@ __device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __re
         const int base = next_base, end = next_end;
         // prefetch the bounds of the following tile while this one streams in
         if (t + 1 < nt) {
-          nb_a = a + kSpTile;
+          nb_a = row_of(t + 1);
           nb_b = min(nb_a + kSpTile, R1);
-          next_base = end;
+          next_base = __ldg(A.rp + nb_a);
           next_end = __ldg(A.rp + nb_b);
         }
         if (t >= kSpStages) mbar_wait(&sm.empty[s], ((t / kSpStages) - 1) & 1);
@@ -389,7 +395,7 @@ __device__ __forceinline__ void spmv_pipeline(const CsrView<T>& A, const T* __re
   const int tid = threadIdx.x;
   for (int t = 0; t < nt; ++t) {
     const int s = t % kSpStages;
-    const long long a = R0 + (long long)t * kSpTile;
+    const long long a = row_of(t);
     const int nrows = (int)min((long long)kSpTile, R1 - a);
     mbar_wait(&sm.full[s], (t / kSpStages) & 1);
     const int base = sm.meta[s][0];

@@ -140,3 +140,15 @@ def test_oracle_equals_reference_directly(reference):
                              (mp.gmres_ir(A, b, criteria=crit), O.solve_ir(Ao, b, m=m))):
                 assert ref.total_iters == ora.total_iters
                 assert np.array_equal(ref.x, ora.x)
+
+
+def test_fd_order_spread_fixture_is_anchored_on_the_reference(golden_runs):
+    """The FD reduction-order study (tests/golden/fd_order_spread.py) starts from
+    the unperturbed oracle, which must reproduce the reference's count."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "fd_order_spread.json")) as f:
+        spread = json.load(f)
+    for name, sp in spread.items():
+        assert sp["counts"]["reference"] == golden_runs[name]["total_iters"]
+        assert sp["min"] <= sp["counts"]["reference"] <= sp["max"]
