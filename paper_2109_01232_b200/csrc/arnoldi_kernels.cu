@@ -489,6 +489,89 @@ __global__ void __launch_bounds__(kThreads) k_dot1_w(const T* __restrict__ w, lo
   }
 }
 
+// ============================= pass-1 dots on a stored w (split K_A, A/B path)
+// c1 = V[:, :k]^T w, w0 = ||w||, finite check (krylov.py:133-139) when the
+// SpMV has already written w (L2-resident at the bench sizes).  Warp w owns
+// basis vectors i = w + 8q (q < KV); blocks of U * 32 * VN rows are dealt
+// round-robin over the grid; warp 0 also accumulates ||w||^2 and the finite
+// flag.  One deterministic CTA reduction + fixed-order last-CTA finalisation.
+template <typename T, int KV, int U>
+__global__ void __launch_bounds__(kThreads) k_dot1_wo(const T* __restrict__ w, long long n,
+                                                      const T* __restrict__ V, long long ldv, int k,
+                                                      StateView<T> sv, WsView ws) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  constexpr int RB = 32 * VN;
+  __shared__ T red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  T acc[KV];
+#pragma unroll
+  for (int q = 0; q < KV; ++q) acc[q] = T(0);
+  T ss = T(0);
+  int bad = 0;
+  for (long long base = (long long)blockIdx.x * U * RB; base < n; base += (long long)gridDim.x * U * RB) {
+    T wv[U][VN], v[U][KV][VN];
+#pragma unroll
+    for (int b = 0; b < U; ++b) {
+      const long long r = base + (long long)b * RB + (long long)lane * VN;
+      const bool in = r < n;   // rows in [n, ldv) are zero padding
+      if (in) vload(w + r, wv[b]);
+      else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) wv[b][e] = T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < KV; ++q) {
+        const int i = warp + kWarps * q;
+        if (in && i < k) vload_cs(V + (size_t)i * ldv + r, v[b][q]);
+        else {
+#pragma unroll
+          for (int e = 0; e < VN; ++e) v[b][q][e] = T(0);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < U; ++b) {
+#pragma unroll
+      for (int q = 0; q < KV; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[b][q][e], wv[b][e], acc[q]);
+      if (warp == 0) {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          ss = fma_rn(wv[b][e], wv[b][e], ss);
+          bad |= !isfinite(wv[b][e]);
+        }
+      }
+    }
+  }
+  const int stride = k + 2;
+  T* part = static_cast<T*>(ws.part);
+#pragma unroll
+  for (int q = 0; q < KV; ++q) {
+    const int i = warp + kWarps * q;
+    const T a = warp_sum(acc[q]);
+    if (lane == 0 && i < k) part[(size_t)blockIdx.x * stride + i] = a;
+  }
+  if (warp == 0) {
+    const T t = warp_sum(ss);
+    const int anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      part[(size_t)blockIdx.x * stride + k] = t;
+      part[(size_t)blockIdx.x * stride + k + 1] = anybad ? T(1) : T(0);
+    }
+  }
+  if (last_cta(ws.counter)) {
+    finalize_columns(part, gridDim.x, stride, k + 2, [&](int c, T s) {
+      if (sv.dist) sv.red[c] = s;
+      else if (c < k) sv.c1[c] = s;
+      else if (c == k) sv.h->w0 = (double)sqrt_rn(s);
+      else if (s != T(0)) { sv.h->flags |= MPG_FLAG_NONFINITE_OP; sv.h->done = 1; }
+    });
+  }
+  (void)red;
+}
+
 // ================================================= K_C update_norm + Givens
 
 // glibc-style hypot for the fp64 rotation (np.hypot -> libm hypot);
@@ -1126,6 +1209,56 @@ cudaError_t launch_dot1_w(const T* w, long long n, const T* V, long long ldv, in
   return cudaGetLastError();
 }
 
+template <typename T, int KV, int U>
+static cudaError_t launch_dot1_wo_k(const T* w, long long n, const T* V, long long ldv, int k,
+                                    StateView<T> sv, WsView ws, cudaStream_t st) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [] {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dot1_wo<T, KV, U>, kThreads, 0);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  const long long blk = (long long)U * 32 * Vec<T>::n;
+  long long G = (n + blk - 1) / blk;
+  const long long cap = std::min<long long>((long long)num_sms() * occ, kMaxParts);
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  count_launch();
+  k_dot1_wo<T, KV, U><<<(unsigned)G, kThreads, 0, st>>>(w, n, V, ldv, k, sv, ws);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_dot1_wo(const T* w, long long n, const T* V, long long ldv, int k,
+                           StateView<T> sv, WsView ws, cudaStream_t st) {
+  switch ((k + kWarps - 1) / kWarps) {
+    case 1: return launch_dot1_wo_k<T, 1, 4>(w, n, V, ldv, k, sv, ws, st);
+    case 2: return launch_dot1_wo_k<T, 2, 4>(w, n, V, ldv, k, sv, ws, st);
+    case 3: return launch_dot1_wo_k<T, 3, 2>(w, n, V, ldv, k, sv, ws, st);
+    case 4: return launch_dot1_wo_k<T, 4, 2>(w, n, V, ldv, k, sv, ws, st);
+    case 5: return launch_dot1_wo_k<T, 5, 2>(w, n, V, ldv, k, sv, ws, st);
+    case 6: return launch_dot1_wo_k<T, 6, 1>(w, n, V, ldv, k, sv, ws, st);
+    case 7: return launch_dot1_wo_k<T, 7, 1>(w, n, V, ldv, k, sv, ws, st);
+    case 8: return launch_dot1_wo_k<T, 8, 1>(w, n, V, ldv, k, sv, ws, st);
+    default: return launch_dot1_w<T>(w, n, V, ldv, k, sv, ws, st);
+  }
+}
+
+// K_A as two launches, SpMV (w written, L2-resident) + k_dot1_wo, is the
+// default: measured on B200 (cfg2, 50-step cycle) 4.80 ms vs 5.53 ms fused in
+// fp32 and 8.93 vs 12.29 ms in fp64 -- the fused kernel's SpMV phase and dot
+// phase serialise inside each CTA and its registers cap occupancy at 3 CTAs/SM.
+// MPG_SPLIT_KA=0 selects the fused kernel (A/B measurement).
+bool split_spmv_dot1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_SPLIT_KA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename T>
 cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,
                                   StateView<T> sv, WsView ws, cudaStream_t st);
@@ -1450,6 +1583,8 @@ cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> 
                                         StateView<T>, WsView, cudaStream_t);                   \
   template cudaError_t launch_update_dot<T>(const T*, long long, long long, int, T*,            \
                                             StateView<T>, WsView, cudaStream_t);               \
+  template cudaError_t launch_dot1_wo<T>(const T*, long long, const T*, long long, int,         \
+                                         StateView<T>, WsView, cudaStream_t);                  \
   template cudaError_t launch_update_norm<T>(const T*, long long, long long, int, T*,           \
                                              StateView<T>, WsView, int, cudaStream_t);         \
   template cudaError_t launch_step_scale<T>(const T*, T*, long long, int, StateView<T>,         \

@@ -274,7 +274,7 @@ static int arnoldi_step_t(int64_t n, int64_t ldv, int32_t m, int32_t j, int32_t 
   WsView w = make_ws(ws);
   T* V = static_cast<T*>(Vp);
   T* wv = static_cast<T*>(wp);
-  cudaError_t e = launch_dot1_w<T>(wv, n, V, ldv, j + 1, sv, w, st);
+  cudaError_t e = launch_dot1_wo<T>(wv, n, V, ldv, j + 1, sv, w, st);
   if (!e) e = launch_update_dot<T>(V, ldv, n, j + 1, wv, sv, w, st);
   if (!e) e = launch_update_norm<T>(V, ldv, n, j, wv, sv, w, m_limit, st);
   if (!e) e = launch_step_scale<T>(wv, V + (size_t)(j + 1) * ldv, n, j, sv, st);

@@ -250,9 +250,14 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       const T* z = nullptr;
       { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
       ProfScope ps(PK_SPMV_DOT);
-      TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
-        return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
-      }));
+      if (split_spmv_dot1()) {
+        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
+        TRY(launch_dot1_wo<T>(wj, d.n, V, d.ldv, j + 1, sv, ws, st));
+      } else {
+        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
+          return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
+        }));
+      }
     }
     { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, wj, sv, ws, st)); }
     if (fuse_update_norm_scale() && !fuse) {
@@ -322,6 +327,12 @@ static cudaError_t enqueue_phase(const mpg_solver& s, int phase, int j, int m_li
     case MPG_PH_START_SCALE:
       return launch_start_scale<T>(static_cast<const T*>(ir ? d.r_in : d.r), V, d.n, sv, st);
     case MPG_PH_SPMV_DOT:
+      if (split_spmv_dot1()) {
+        TRY(with_matrix<T>(d, static_cast<const T*>(d.values), d.dia, [&](const auto& A) {
+          return launch_spmv<T>(A, V + (size_t)j * d.ldv, w, ws, st);
+        }));
+        return launch_dot1_wo<T>(w, d.n, V, d.ldv, j + 1, sv, ws, st);
+      }
       return with_matrix<T>(d, static_cast<const T*>(d.values), d.dia, [&](const auto& A) {
         return launch_spmv_dot1<T>(A, V + (size_t)j * d.ldv, w, V, d.ldv, j + 1, sv, ws, st);
       });

@@ -46,10 +46,14 @@ __device__ __forceinline__ T xload(const T* __restrict__ x, long long c, bool sc
   return scaled ? div_rn(v, h) : v;
 }
 
+// largest tile any pipeline hands to an epilogue (the vectorised stencil loop:
+// kSpConsumers threads x one 16-byte row group)
+constexpr int kStTileMax = kSpConsumers * 4;
+
 // shared memory the epilogues use (tile of SpMV results + reduction scratch)
 template <typename T>
 struct alignas(16) EpiShared {
-  alignas(16) T ys[2][kSpTile];
+  alignas(16) T ys[2][kStTileMax];
   T red[32];
   T acc[8];
 };
@@ -298,6 +302,102 @@ __device__ __forceinline__ void stencil_loop(long long n, E& epi, EpiShared<T>& 
   epi.on_end();
 }
 
+// Epilogues may take a whole 16-byte row group at once (kVecRows + on_rows);
+// otherwise the group is handed over row by row.
+template <typename E, typename = void> struct has_vec_rows { static constexpr bool value = false; };
+template <typename E> struct has_vec_rows<E, decltype((void)E::kVecRows)> {
+  static constexpr bool value = E::kVecRows;
+};
+template <typename T, typename E>
+__device__ __forceinline__ void epi_rows(E& epi, long long r0, T (&y)[Vec<T>::n], int cnt, T* ysp) {
+  if constexpr (has_vec_rows<E>::value) {
+    epi.on_rows(r0, y, cnt, ysp);
+  } else {
+    for (int e = 0; e < cnt; ++e) ysp[e] = epi.on_row(r0 + e, y[e]);
+  }
+}
+
+// x[p .. p + VN) for a uniform misalignment `mis` = (p mod VN) (r0 is VN-aligned)
+template <typename T>
+__device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)[Vec<T>::n]) {
+  constexpr int VN = Vec<T>::n;
+  if (mis == 0) {
+    vload(p, o);
+  } else if (VN == 4 && mis == 2) {
+    const float2 a = __ldg(reinterpret_cast<const float2*>(p));
+    const float2 b = __ldg(reinterpret_cast<const float2*>(p + 2));
+    o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < VN; ++e) o[e] = __ldg(p + e);
+  }
+}
+
+// Vectorised branchless stencil rows on padded inputs: each consumer thread
+// owns one 16-byte group of VN consecutive rows.  Per group: S 16-byte value
+// loads (slot-major storage is VN-aligned), one 16-byte load of x[r0..] that
+// also feeds the +-1 neighbours (plus one scalar each), and one window load
+// per +-nx / +-nx^2 neighbour (16-byte when aligned).  The per-row reduction is
+// stencil_row_padded's: add.reduceat order over the present slots, bit-exact.
+template <typename T, int S, typename E>
+__device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const T* __restrict__ x,
+                                                 const long long (&off)[S], E& epi,
+                                                 EpiShared<T>& es) {
+  constexpr int VN = Vec<T>::n;
+  constexpr int TILE = kSpConsumers * VN;
+  constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
+  const long long n = SV.n;
+  const size_t ld = (size_t)SV.ldv;
+  int mis[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) mis[s] = (int)(((off[s] % VN) + VN) % VN);
+  const long long ntiles = (n + TILE - 1) / TILE;
+  int t = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+    const long long a = tile * TILE;
+    const int nrows = (int)min((long long)TILE, n - a);
+    T* ys = es.ys[t & 1];
+    const int rr = threadIdx.x * VN;
+    if (rr < nrows) {
+      const long long r0 = a + rr;
+      T pv[S][VN], px[S][VN];
+#pragma unroll
+      for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
+      vload(x + r0, px[C]);
+      const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
+#pragma unroll
+      for (int s = 0; s < S; ++s)
+        if (s < C - 1 || s > C + 1) xwindow(x + r0 + off[s], mis[s], px[s]);
+      px[C - 1][0] = xm;
+#pragma unroll
+      for (int e = 1; e < VN; ++e) px[C - 1][e] = px[C][e - 1];
+#pragma unroll
+      for (int e = 0; e < VN - 1; ++e) px[C + 1][e] = px[C][e + 1];
+      px[C + 1][VN - 1] = xp;
+      T y[VN];
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        bool have = false;
+        T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          const T p = mul_rn(pv[s][e], px[s][e]);
+          const bool pr = present(pv[s][e]);
+          const T nrest = add_rn(rest, p);
+          rest = (pr && have) ? nrest : rest;
+          p0 = (pr && !have) ? p : p0;
+          have = have || pr;
+        }
+        y[e] = add_rn(p0, rest);
+      }
+      epi_rows(epi, r0, y, min(VN, nrows - rr), ys + rr);
+    }
+    consumer_sync();
+    epi.on_tile(a, nrows, ys);
+  }
+  epi.on_end();
+}
+
 template <typename T, typename E>
 __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
                                                  E& epi, EpiShared<T>& es) {
@@ -309,14 +409,10 @@ __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const 
     const long long nx = S.nx, p2 = nx * nx;
     if (S.dims == 3) {
       const long long off[7] = {-p2, -nx, -1, 0, 1, nx, p2};
-      stencil_loop(n, epi, es, [&](long long r) {
-        return stencil_row_padded<T, 7, false>(S.vals + r, ld, x + r, off, hdiv);
-      });
+      stencil_loop_vec<T, 7>(S, x, off, epi, es);
     } else {
       const long long off[5] = {-nx, -1, 0, 1, nx};
-      stencil_loop(n, epi, es, [&](long long r) {
-        return stencil_row_padded<T, 5, false>(S.vals + r, ld, x + r, off, hdiv);
-      });
+      stencil_loop_vec<T, 5>(S, x, off, epi, es);
     }
   } else if (scaled) {
     stencil_loop(n, epi, es, [&](long long r) { return stencil_row<T, true>(S, x, r, hdiv); });

@@ -47,6 +47,11 @@ struct EpiPlain {
   __device__ bool skip() const { return false; }
   __device__ void init(EpiShared<T>&, unsigned char*) {}
   __device__ T on_row(long long r, T v) { y[r] = v; return v; }
+  static constexpr bool kVecRows = true;
+  __device__ void on_rows(long long r0, T (&v)[Vec<T>::n], int cnt, T*) {
+    if (cnt == Vec<T>::n) vstore(y + r0, v);
+    else for (int e = 0; e < cnt; ++e) y[r0 + e] = v[e];
+  }
   __device__ void on_tile(long long, int, const T*) {}
   __device__ void on_end() {}
 };
@@ -196,10 +201,25 @@ struct EpiDot1Warp {
     bad |= !isfinite(y);
     return y;
   }
+  // one 16-byte row group (vectorised stencil loop; never with fused scaling)
+  static constexpr bool kVecRows = true;
+  __device__ void on_rows(long long r0, T (&y)[VN], int cnt, T* ysp) {
+    if (cnt == VN) {
+      vstore(w + r0, y);
+      vstore(ysp, y);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        ss = fma_rn(y[e], y[e], ss);
+        bad |= !isfinite(y[e]);
+      }
+    } else {
+      for (int e = 0; e < cnt; ++e) ysp[e] = on_row(r0 + e, y[e]);
+    }
+  }
   __device__ void on_tile(long long a, int nr, const T* ys) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-    for (int g = 0; g < kSpTile / RB; ++g) {
+    for (int g = 0; g < kStTileMax / RB; ++g) {
       const int r0 = g * RB + lane * VN;
       if (r0 + VN <= nr) {
         T y[VN];
@@ -419,7 +439,9 @@ static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& e
     cudaGetLastError();
     if (occ < 1) occ = 1;
   });
-  long long tiles = (S.n + kSpTile - 1) / kSpTile;
+  // the padded (branchless) path deals tiles of one 16-byte row group per thread
+  const long long tile_rows = S.padded && !S.xdiv ? (long long)kSpConsumers * Vec<T>::n : kSpTile;
+  long long tiles = (S.n + tile_rows - 1) / tile_rows;
   long long G = (long long)num_sms() * occ;
   if (tiles < G) G = tiles;
   if (G > kMaxParts) G = kMaxParts;

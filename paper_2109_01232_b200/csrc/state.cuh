@@ -114,6 +114,10 @@ template <typename T>
 cudaError_t launch_dot1_w(const T* w, long long n, const T* V, long long ldv, int k,
                           StateView<T> sv, WsView ws, cudaStream_t st);
 template <typename T>
+cudaError_t launch_dot1_wo(const T* w, long long n, const T* V, long long ldv, int k,
+                           StateView<T> sv, WsView ws, cudaStream_t st);
+bool split_spmv_dot1();
+template <typename T>
 cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* w,
                               StateView<T> sv, WsView ws, cudaStream_t st);
 template <typename T>
