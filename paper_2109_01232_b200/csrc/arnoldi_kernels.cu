@@ -420,21 +420,15 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__
   for (int q = 0; q < KV; ++q) {
     const int i = warp + kWarps * q;
     const T a = warp_sum(acc[q]);
-    if (lane == 0 && i < k) part[(size_t)blockIdx.x * k + i] = a;
+    if (lane == 0 && i < k) part[(size_t)i * kMaxParts + blockIdx.x] = a;
   }
-  if (last_cta(ws.counter)) {
-    const int jj = k - 1;
-    for (int c = warp; c < k; c += kWarps) {
-      T s2 = T(0);
-      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
-        sv.c2[c] = s2;
-        sv.Hc(jj, c) = add_rn(add_rn(T(0), sv.c1[c]), s2);   // h = 0; h += c1; h += c2
-      }
-    }
-  }
+  const int jj = k - 1;
+  grid_reduce_cols<kRedGroup>(part, kMaxParts, static_cast<T*>(ws.gpart), ws.gcount, k,
+                              [&](int c, T s2) {
+    if (sv.dist) { sv.red[c] = s2; return; }   // raw local sum (distributed)
+    sv.c2[c] = s2;
+    sv.Hc(jj, c) = add_rn(add_rn(T(0), sv.c1[c]), s2);   // h = 0; h += c1; h += c2
+  });
 }
 
 // ================================== generic-operator pass-1 dots (no SpMV)
@@ -545,30 +539,29 @@ __global__ void __launch_bounds__(kThreads) k_dot1_wo(const T* __restrict__ w, l
       }
     }
   }
-  const int stride = k + 2;
+  // column-major partials (c1[0..k), ||w||^2, non-finite), two-level reduction
   T* part = static_cast<T*>(ws.part);
 #pragma unroll
   for (int q = 0; q < KV; ++q) {
     const int i = warp + kWarps * q;
     const T a = warp_sum(acc[q]);
-    if (lane == 0 && i < k) part[(size_t)blockIdx.x * stride + i] = a;
+    if (lane == 0 && i < k) part[(size_t)i * kMaxParts + blockIdx.x] = a;
   }
   if (warp == 0) {
     const T t = warp_sum(ss);
     const int anybad = __any_sync(0xffffffffu, bad);
     if (lane == 0) {
-      part[(size_t)blockIdx.x * stride + k] = t;
-      part[(size_t)blockIdx.x * stride + k + 1] = anybad ? T(1) : T(0);
+      part[(size_t)k * kMaxParts + blockIdx.x] = t;
+      part[(size_t)(k + 1) * kMaxParts + blockIdx.x] = anybad ? T(1) : T(0);
     }
   }
-  if (last_cta(ws.counter)) {
-    finalize_columns(part, gridDim.x, stride, k + 2, [&](int c, T s) {
-      if (sv.dist) sv.red[c] = s;
-      else if (c < k) sv.c1[c] = s;
-      else if (c == k) sv.h->w0 = (double)sqrt_rn(s);
-      else if (s != T(0)) { sv.h->flags |= MPG_FLAG_NONFINITE_OP; sv.h->done = 1; }
-    });
-  }
+  grid_reduce_cols<kRedGroup>(part, kMaxParts, static_cast<T*>(ws.gpart), ws.gcount, k + 2,
+                              [&](int c, T s) {
+    if (sv.dist) sv.red[c] = s;
+    else if (c < k) sv.c1[c] = s;
+    else if (c == k) sv.h->w0 = (double)sqrt_rn(s);
+    else if (s != T(0)) { sv.h->flags |= MPG_FLAG_NONFINITE_OP; sv.h->done = 1; }
+  });
   (void)red;
 }
 

@@ -68,18 +68,28 @@ inline StateView<T> make_state(void* base, int m) {
 constexpr int kMaxM = 512;                       // largest restart length supported
 constexpr int kMaxParts = 148 * 8;               // partial rows (CTAs) per reduction
 constexpr int64_t kWsCounterBytes = 256;
-constexpr int64_t kWsBytes = kWsCounterBytes + (int64_t)kMaxParts * (kMaxM + 8) * 8 + 4096;
+// two-level grid reductions (grid_reduce_cols): CTAs are grouped by kRedGroup
+constexpr int kRedGroup = 32;
+constexpr int kRedGroups = (kMaxParts + kRedGroup - 1) / kRedGroup;   // 37
+constexpr int64_t kPartBytes = (int64_t)kMaxParts * (kMaxM + 8) * 8;
+constexpr int64_t kGPartBytes = (int64_t)64 * (kMaxM + 8) * 8;
+constexpr int64_t kWsBytes = kWsCounterBytes + kPartBytes + kGPartBytes + 4096;
 
 struct WsView {
   unsigned int* counter;   // one election counter (kernels on a stream are serial)
   int64_t* scratch_i64;    // small integer scratch (overflow index etc.)
-  void* part;              // partials, [parts][stride] of T
+  void* part;              // partials, [parts][stride] of T (column-major [c][kMaxParts] for grid_reduce_cols)
+  void* gpart;             // group partials [c][64] (grid_reduce_cols)
+  unsigned int* gcount;    // per-group arrival counters [64] (grid_reduce_cols)
 };
 inline WsView make_ws(void* base) {
   WsView w;
-  w.counter = static_cast<unsigned int*>(base);
-  w.scratch_i64 = reinterpret_cast<int64_t*>(static_cast<char*>(base) + 128);
-  w.part = static_cast<char*>(base) + kWsCounterBytes;
+  char* b = static_cast<char*>(base);
+  w.counter = reinterpret_cast<unsigned int*>(b);
+  w.scratch_i64 = reinterpret_cast<int64_t*>(b + 128);
+  w.part = b + kWsCounterBytes;
+  w.gpart = b + kWsCounterBytes + kPartBytes;
+  w.gcount = reinterpret_cast<unsigned int*>(b + kWsCounterBytes + kPartBytes + kGPartBytes);
   return w;
 }
 
