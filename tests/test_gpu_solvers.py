@@ -323,3 +323,39 @@ def test_cfg2_laplace3d150_full_solve_vs_reference(solver, cfg2_reference):
     ref = np.asarray(g["x_sample"])
     assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-8
     assert abs(float(torch.linalg.norm(rep.x)) - g["x_norm"]) / g["x_norm"] <= 1e-8
+
+
+@pytest.fixture(scope="module")
+def cfg3_reference():
+    from conftest import load_json
+    return load_json("reference_cfg3.json")["runs"]
+
+
+@pytest.mark.parametrize("solver", ["ir+jacobi1", "fp64"])
+def test_cfg3_convdiff1500_full_solve_vs_reference(solver, cfg3_reference):
+    """BASELINE configs[2] at full size (UniFlow2D = convdiff2d:1500 with
+    convection 1501, 2.25M rows, nonsymmetric) against the reference's own run
+    (tests/golden/reference_cfg3.json: 2744 fp64 / 3100 IR + fp32 Jacobi(1)
+    iterations, ~14 CPU-minutes each): same count (+-2 % or the marginal-cycle
+    rule), boundary residuals within 2x, final fp64 residual <= 1e-10,
+    solution within 1e-8 relative on the strided sample."""
+    g = cfg3_reference[f"convdiff2d:1500:c1501/{solver}/m50"]
+    A = P.generate(P.StencilSpec(P.StencilKind.CONVDIFF2D, 1500, convection=1501.0))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    crit = P.StopCriteria(rtol=1e-10, m=50)
+    if solver == "fp64":
+        rep = P.gmres_restarted(A, b, criteria=crit)
+    else:
+        M = P.build_block_jacobi(P.convert_matrix(A, P.FP32), 1)
+        rep = P.gmres_ir(A, b, criteria=crit, precond_fp32=M)
+    assert rep.converged
+    assert iters_match(rep, g, 50), (rep.total_iters, g["total_iters"], g["boundaries"][-3:])
+    ours = {e.iteration: e.explicit for e in rep.residual_history if e.explicit is not None}
+    for it, _, ref_exp, _ in g["boundaries"]:
+        if it in ours and it > 0:
+            assert 0.5 <= ours[it] / ref_exp <= 2.0, (it, ours[it], ref_exp)
+    nr, _ = P.explicit_residual(A, b, rep.x)
+    assert nr / float(torch.linalg.norm(b)) <= 1e-10
+    x = rep.x.cpu().numpy()[:: g["x_stride"]]
+    ref = np.asarray(g["x_sample"])
+    assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-8
