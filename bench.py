@@ -115,6 +115,17 @@ def cycle_bytes(n: int, nnz: int, m: int, s: int, storage: str = "csr") -> dict[
     }
 
 
+def split_cycle_bytes(model: dict, n: int, nnz: int, m: int, s: int, storage: str) -> dict:
+    """K_A split into two launches (the default): the SpMV class moves the
+    matrix, x once and w once; the pass-1 dot kernel reads V[0..k) and w.
+    Kernel-level algorithmic bytes: each launch's inputs and outputs once."""
+    spmv = (nnz * s if storage == "stencil" else nnz * (s + 4) + 4 * (n + 1)) + 2 * n * s
+    out = dict(model)
+    out["spmv_dot1"] = m * spmv
+    out["dot1"] = sum((k + 1) * n * s for k in range(1, m + 1))
+    return out
+
+
 def native_arm(args, rank: int, world: int):
     import numpy as np
     import torch
@@ -191,6 +202,8 @@ def native_arm(args, rank: int, world: int):
         used = ns.storage
         ns.close()
         model = cycle_bytes(n, nnz, M, 4, used)
+        if prof.get("dot1", (0.0, 0))[1] > 0:
+            model = split_cycle_bytes(model, n, nnz, M, 4, used)
         if prof.get("scale", (0.0, 0))[1] == 0:
             # K_S fused into K_C (k_update_norm_scale): read V + w', write v = (k+2) n s,
             # the same count as update_norm_givens; no separate scale traffic
@@ -258,13 +271,29 @@ def native_arm(args, rank: int, world: int):
         "profile_cycle_csr": profiles["csr"],
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(dom_gbs, 1), "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": round(dom_gbs / peak, 4),
-                     "traffic": None},
+                     "algorithmic_bytes_per_launch": round(model[dom] / prof[dom][1]),
+                     "launches_per_cycle": prof[dom][1],
+                     **_traffic(dom)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": {"value": round(e2e_s, 5), "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "iters": rep_h.total_iters},
     }
     return out
+
+
+def _traffic(cls: str) -> dict:
+    """DRAM bytes per launch of kernel class `cls` from the committed ncu capture
+    of one cfg2 IR cycle (tools/traffic_from_ncu.py; L2 flushed per launch)."""
+    path = os.path.join(ROOT, "profiles", "r1_traffic_ir_cycle.json")
+    try:
+        with open(path) as f:
+            c = json.load(f)["classes"][cls]
+        return {"traffic": round(c["dram_bytes_per_launch"]),
+                "traffic_source": "profiles/r1_traffic_ir_cycle.json (ncu dram__bytes_read+write, "
+                                  "mean over the cycle's launches)"}
+    except (OSError, KeyError, ValueError):
+        return {"traffic": None}
 
 
 def _backend() -> str:

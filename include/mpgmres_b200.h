@@ -330,10 +330,11 @@ int mpg_solver_begin(mpg_solver* s, void* stream);
 int mpg_solver_cycle(mpg_solver* s, int32_t m_limit, void* stream);
 /* Profiling variant of mpg_solver_cycle: launches the same kernels eagerly
  * with CUDA events around each kernel class, synchronises, and writes the
- * summed milliseconds (and launch-group counts) per class into ms_out[8] /
- * launches_out[8]: 0 start, 1 preconditioner, 2 SpMV + CGS pass-1 dots,
- * 3 CGS update + pass-2 dots, 4 CGS update + norm + Givens, 5 basis scale,
- * 6 back-solve + solution update, 7 explicit residual. */
+ * summed milliseconds (and launch-group counts) per class into ms_out[9] /
+ * launches_out[9]: 0 start, 1 preconditioner, 2 SpMV (+ CGS pass-1 dots when
+ * fused, MPG_SPLIT_KA=0), 3 CGS update + pass-2 dots, 4 CGS update + norm +
+ * Givens (+ basis scale when fused), 5 basis scale, 6 back-solve + solution
+ * update, 7 explicit residual, 8 CGS pass-1 dots (split K_A, the default). */
 int mpg_solver_profile_cycle(mpg_solver* s, int32_t m_limit, void* stream, double* ms_out,
                              int32_t* launches_out);
 /* Enqueue one phase of a distributed cycle (desc.dist = 1); j = Arnoldi

@@ -102,7 +102,8 @@ _SIGS = {
     "mpg_solver_profile_cycle": (C.c_int, [_vp, _i32, _vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
 }
 PROFILE_CLASSES = ("start", "precond", "spmv_dot1", "update_dot", "update_norm_givens",
-                   "scale", "finish", "residual")
+                   "scale", "finish", "residual", "dot1")
+# with K_A split (the default) "spmv_dot1" times the SpMV alone and "dot1" the pass-1 dots
 
 _LIB = None
 _ERR: str | None = None

@@ -44,7 +44,7 @@ struct ProfScope {
   }
 };
 enum { PK_START = 0, PK_PRECOND, PK_SPMV_DOT, PK_UPDATE_DOT, PK_UPDATE_NORM, PK_SCALE, PK_FINISH,
-       PK_RESIDUAL, PK_COUNT };
+       PK_RESIDUAL, PK_DOT1, PK_COUNT };   // PK_SPMV_DOT: the SpMV alone when K_A is split
 
 #define TRY(...)                       \
   do {                                   \
@@ -249,11 +249,15 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       const T* vj = V + (size_t)j * d.ldv;
       const T* z = nullptr;
       { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
-      ProfScope ps(PK_SPMV_DOT);
       if (split_spmv_dot1()) {
-        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
+        {
+          ProfScope ps(PK_SPMV_DOT);
+          TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
+        }
+        ProfScope ps(PK_DOT1);
         TRY(launch_dot1_wo<T>(wj, d.n, V, d.ldv, j + 1, sv, ws, st));
       } else {
+        ProfScope ps(PK_SPMV_DOT);
         TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
           return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
         }));

@@ -316,8 +316,8 @@ class NativeSolve:
 
     def profile_cycle(self, m_limit: int) -> dict[str, tuple[float, int]]:
         """One eager cycle with per-kernel-class CUDA events: {class: (ms, launches)}."""
-        ms = (C.c_double * 8)()
-        cnt = (C.c_int32 * 8)()
+        ms = (C.c_double * 16)()
+        cnt = (C.c_int32 * 16)()
         _lib.call("mpg_solver_profile_cycle", self.handle, int(m_limit), stream_handle(), ms, cnt)
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(_lib.PROFILE_CLASSES)}
 
