@@ -12,7 +12,8 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpgmres_b200.so")
+# MPG_LIB_PATH: an alternative build of the same library (kernel A/B variants, tools/)
+LIB_PATH = os.environ.get("MPG_LIB_PATH") or os.path.join(_HERE, "libmpgmres_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mpgmres_b200.h")
 
 FP32, FP64 = 0, 1

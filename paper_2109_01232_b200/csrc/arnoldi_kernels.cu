@@ -327,9 +327,20 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_q(const T* __restrict__
 // w' = w - u and the lane's KV pass-2 accumulators.  V is read once; per
 // lane registers hold KV slices and KV accumulators.
 template <typename T, int KV>
-__global__ void __launch_bounds__(kThreads) k_update_dot_w(const T* __restrict__ V, long long ldv,
+#ifndef MPG_KB_MINB
+#define MPG_KB_MINB 4   // measured: 4 CTAs/SM (<= 64 regs) beats the unbounded 74-reg build
+#endif
+#ifndef MPG_KA2_MINB
+#define MPG_KA2_MINB 1
+#endif
+#ifndef MPG_KCS_MINB
+#define MPG_KCS_MINB 1
+#endif
+__global__ void __launch_bounds__(kThreads, MPG_KB_MINB) k_update_dot_w(const T* __restrict__ V, long long ldv,
                                                            long long n, int k, T* __restrict__ w,
                                                            StateView<T> sv, WsView ws) {
+  pdl_wait();
+  pdl_trigger();
   if (gated(sv.h)) return;
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
@@ -490,9 +501,11 @@ __global__ void __launch_bounds__(kThreads) k_dot1_w(const T* __restrict__ w, lo
 // round-robin over the grid; warp 0 also accumulates ||w||^2 and the finite
 // flag.  One deterministic CTA reduction + fixed-order last-CTA finalisation.
 template <typename T, int KV, int U>
-__global__ void __launch_bounds__(kThreads) k_dot1_wo(const T* __restrict__ w, long long n,
+__global__ void __launch_bounds__(kThreads, MPG_KA2_MINB) k_dot1_wo(const T* __restrict__ w, long long n,
                                                       const T* __restrict__ V, long long ldv, int k,
                                                       StateView<T> sv, WsView ws) {
+  pdl_wait();
+  pdl_trigger();
   if (gated(sv.h)) return;
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
@@ -772,10 +785,12 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
 }
 
 template <typename T, bool CACHE>
-__global__ void __launch_bounds__(kThreads) k_update_norm_scale(const T* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(const T* __restrict__ V, long long ldv,
                                                                 long long n, int j, T* __restrict__ w,
                                                                 StateView<T> sv, WsView ws, int m_limit,
                                                                 int kpad) {
+  pdl_wait();
+  pdl_trigger();
   if (gated(sv.h)) return;
   constexpr int VN = Vec<T>::n;
   const int k = j + 1;
@@ -1162,6 +1177,27 @@ __global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, l
 // ================================================================= launchers
 
 // MPG_FUSE_CS=0 selects the separate K_C + K_S launches (A/B measurement)
+// Off by default: measured no change on the graph-replayed cfg2 solve
+// (0.513 s vs 0.515 s); MPG_PDL=1 enables it for A/B runs.
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// PDL on the cooperative K_CS launch (MPG_KCS_PDL=0 to disable)
+static bool kcs_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_KCS_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool fuse_update_norm_scale() {
   static int v = -1;
   if (v < 0) {
@@ -1218,8 +1254,8 @@ static cudaError_t launch_dot1_wo_k(const T* w, long long n, const T* V, long lo
   if (G > cap) G = cap;
   if (G < 1) G = 1;
   count_launch();
-  k_dot1_wo<T, KV, U><<<(unsigned)G, kThreads, 0, st>>>(w, n, V, ldv, k, sv, ws);
-  return cudaGetLastError();
+  return launch_k(true, false, k_dot1_wo<T, KV, U>, dim3((unsigned)G), dim3(kThreads), 0, st, w, n, V, ldv,
+                  k, sv, ws);
 }
 
 template <typename T>
@@ -1310,8 +1346,8 @@ static cudaError_t launch_update_dot_w(const T* V, long long ldv, long long n, i
   if (G > cap) G = cap;
   if (G < 1) G = 1;
   count_launch();
-  k_update_dot_w<T, KV><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
-  return cudaGetLastError();
+  return launch_k(true, false, k_update_dot_w<T, KV>, dim3((unsigned)G), dim3(kThreads), 0, st, V, ldv, n,
+                  k, w, sv, ws);
 }
 
 template <typename T>
@@ -1478,20 +1514,13 @@ cudaError_t launch_update_norm_scale(const T* V, long long ldv, long long n, int
     return launch_step_scale<T>(w, const_cast<T*>(V) + (size_t)(j + 1) * ldv, n, j, sv, st);
   }
   const int kpad = (sv.m + 16) & ~7;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = p.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   count_launch();
+  const bool pdl = kcs_pdl();
   if (p.cache)
-    return cudaLaunchKernelEx(&cfg, k_update_norm_scale<T, true>, V, ldv, n, j, w, sv, ws, m_limit, kpad);
-  return cudaLaunchKernelEx(&cfg, k_update_norm_scale<T, false>, V, ldv, n, j, w, sv, ws, m_limit, kpad);
+    return launch_k(pdl, true, k_update_norm_scale<T, true>, dim3(p.grid), dim3(kThreads), p.smem, st, V, ldv,
+                    n, j, w, sv, ws, m_limit, kpad);
+  return launch_k(pdl, true, k_update_norm_scale<T, false>, dim3(p.grid), dim3(kThreads), p.smem, st, V, ldv,
+                  n, j, w, sv, ws, m_limit, kpad);
 }
 
 template <typename T>

@@ -312,8 +312,45 @@ __device__ __forceinline__ T row_reduce(const Get& get, int len) {
 }
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL).  Kernels of the Arnoldi step are
+// launched with programmatic stream serialisation: a kernel may be scheduled
+// while its predecessor drains, runs until pdl_wait() (griddepcontrol.wait:
+// returns once the predecessor grid has completed and its writes are
+// visible; a no-op for a normal launch), and lets its own successor launch
+// early with pdl_trigger().  Every kernel launched with launch_k(pdl = true)
+// calls pdl_wait() before it reads anything a predecessor wrote.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
 // launch helpers (host)
 int num_sms();
 int grid_for(long long rows, int rows_per_tile, int ctas_per_sm);
+bool pdl_enabled();   // MPG_PDL=0 disables programmatic dependent launches
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, bool coop, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                            size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl && pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 }  // namespace mpg

@@ -43,6 +43,7 @@ __device__ __forceinline__ void consumers_finalize(const T* part, int nparts, in
 
 template <typename T>
 struct EpiPlain {
+  static constexpr bool kPdl = true;   // the Arnoldi-step SpMV (split K_A)
   T* y;
   __device__ bool skip() const { return false; }
   __device__ void init(EpiShared<T>&, unsigned char*) {}
@@ -59,6 +60,7 @@ struct EpiPlain {
 // explicit_residual (solvers.py:443-453): r = b - A x, ||r||
 template <typename T>
 struct EpiResid {
+  static constexpr bool kPdl = false;
   const T* b;
   T* r;
   double* out;
@@ -98,6 +100,7 @@ struct EpiResid {
 // K_A: w = A x; w0 = ||w||; finite check; c1 = V[:, :k]^T w  (krylov.py:128-139)
 template <typename T>
 struct EpiDot1 {
+  static constexpr bool kPdl = false;
   T* w;
   const T* V;
   long long ldv;
@@ -167,6 +170,7 @@ struct EpiDot1 {
 // = 512 contiguous bytes of one vector) into KV per-lane accumulators.
 template <typename T, int KV>
 struct EpiDot1Warp {
+  static constexpr bool kPdl = false;
   static constexpr int VN = 16 / (int)sizeof(T);
   static constexpr int RB = 32 * VN;
   T* w;
@@ -290,6 +294,7 @@ struct EpiDot1Warp {
 // `x` of the pipeline; other operands are own-row elementwise.
 template <typename T>
 struct EpiPoly {
+  static constexpr bool kPdl = false;
   int op;
   T a, b;
   const T* src;   // SpMV input (also own-row operand)
@@ -336,6 +341,8 @@ struct EpiPoly {
 template <typename T, typename E>
 __global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __restrict__ x, E epi) {
   extern __shared__ __align__(128) unsigned char smraw[];
+  pdl_wait();
+  pdl_trigger();
   if (epi.skip()) return;
   SpSmem<T>& sm = *reinterpret_cast<SpSmem<T>*>(smraw);
   epi.init(sm.es, smraw + sizeof(SpSmem<T>));
@@ -347,6 +354,8 @@ __global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, cons
                                                           E epi) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ EpiShared<T> es;
+  pdl_wait();
+  pdl_trigger();
   if (epi.skip()) return;
   epi.init(es, smraw);
   stencil_pipeline(S, x, epi, es);
@@ -423,8 +432,7 @@ static cudaError_t launch_matrix(const CsrView<T>& A, const T* x, const E& epi, 
   if (tiles < G) G = tiles;
   if (G < 1) G = 1;
   count_launch();
-  k_spmv<T, E><<<(unsigned)G, kSpThreads, smem, st>>>(A, x, epi);
-  return cudaGetLastError();
+  return launch_k(E::kPdl, false, k_spmv<T, E>, dim3((unsigned)G), dim3(kSpThreads), smem, st, A, x, epi);
 }
 
 template <typename T, typename E>
@@ -447,8 +455,7 @@ static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& e
   if (G > kMaxParts) G = kMaxParts;
   if (G < 1) G = 1;
   count_launch();
-  k_stencil<T, E><<<(unsigned)G, kSpConsumers, extra, st>>>(S, x, epi);
-  return cudaGetLastError();
+  return launch_k(E::kPdl, false, k_stencil<T, E>, dim3((unsigned)G), dim3(kSpConsumers), extra, st, S, x, epi);
 }
 
 template <typename T, typename M>
