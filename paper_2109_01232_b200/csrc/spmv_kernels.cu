@@ -334,6 +334,62 @@ struct EpiPoly {
         return v;
     }
   }
+  // one 16-byte row group (vectorised stencil loop): the same per-row
+  // arithmetic with 16-byte loads/stores of the own-row operands
+  static constexpr int VN = Vec<T>::n;
+  static constexpr bool kVecRows = true;
+  __device__ void on_rows(long long r0, T (&v)[VN], int cnt, T*) {
+    if (cnt != VN) {
+      for (int e = 0; e < cnt; ++e) on_row(r0 + e, v[e]);
+      return;
+    }
+    T o[VN];
+    switch (op) {
+      case MPG_POLY_HORNER: {
+        T xx[VN];
+        vload(x2 + r0, xx);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) o[e] = add_rn(v[e], mul_rn(a, xx[e]));
+        break;
+      }
+      case MPG_POLY_NEWTON_REAL: {
+        T p[VN], yy[VN];
+        vload(src + r0, p);
+        vload_smem(y + r0, yy);   // plain load: y is read and written by this thread only
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          yy[e] = add_rn(yy[e], mul_rn(a, p[e]));
+          o[e] = sub_rn(p[e], mul_rn(a, v[e]));
+        }
+        vstore(y + r0, yy);
+        break;
+      }
+      case MPG_POLY_PAIR1: {
+        T p[VN], yy[VN];
+        vload(src + r0, p);
+        vload_smem(y + r0, yy);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          yy[e] = add_rn(yy[e], sub_rn(mul_rn(a, p[e]), mul_rn(b, v[e])));
+          o[e] = v[e];
+        }
+        vstore(y + r0, yy);
+        break;
+      }
+      case MPG_POLY_PAIR2: {
+        T p[VN], xx[VN];
+        vload(src + r0, p);
+        vload(x2 + r0, xx);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) o[e] = add_rn(sub_rn(xx[e], mul_rn(a, p[e])), mul_rn(b, v[e]));
+        break;
+      }
+      default:
+#pragma unroll
+        for (int e = 0; e < VN; ++e) o[e] = v[e];
+    }
+    vstore(dst + r0, o);
+  }
   __device__ void on_tile(long long, int, const T*) {}
   __device__ void on_end() {}
 };
