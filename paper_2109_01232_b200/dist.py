@@ -107,6 +107,11 @@ class Collectives:
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        # NCCL collectives are stream-ordered device work: a cycle can be graph-captured
+        try:
+            self.capturable = dist.get_backend(group) == "nccl"
+        except Exception:  # pragma: no cover
+            self.capturable = False
 
     def allreduce_(self, t: torch.Tensor) -> None:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
@@ -132,6 +137,12 @@ class HostStagedCollectives(Collectives):
     """Collectives for a gloo group with device tensors (host-staged copies):
     lets several ranks share one GPU in tests, and runs on CPU tensors too."""
 
+    capturable = False
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self.capturable = False
+
     def allreduce_(self, t: torch.Tensor) -> None:
         h = t.detach().to("cpu", copy=True)
         super().allreduce_(h)
@@ -150,6 +161,8 @@ class HostStagedCollectives(Collectives):
 class NullCollectives:
     """World size 1: the sum over one rank is the identity, no neighbours."""
 
+    capturable = True
+
     def allreduce_(self, t: torch.Tensor) -> None:
         return None
 
@@ -166,11 +179,15 @@ class DistributedStencilSolver:
     for the rank's rows, packed with mpg_stencil_pack_rows)."""
 
     def __init__(self, spec, part: RowPartition, mode: str, m: int, rtol: float,
-                 collectives, precision: Precision = FP64, b_local=None):
+                 collectives, precision: Precision = FP64, b_local=None, use_graph: bool = True):
         from .gen import generate_rows
         if mode not in ("ir", "restarted"):
             raise ValueError("mode must be 'ir' or 'restarted'")
         self.spec, self.part, self.m, self.rtol, self.coll = spec, part, m, rtol, collectives
+        # CUDA-graph replay of whole cycles needs stream-ordered device collectives
+        self.use_graph = bool(getattr(collectives, "capturable", False)) and use_graph
+        self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._eager_cycles: dict[int, int] = {}
         self.mode = _lib.MODE_IR if mode == "ir" else _lib.MODE_RESTARTED
         self.prec = FP32 if mode == "ir" else precision
         outer = FP64 if mode == "ir" else precision
@@ -275,6 +292,39 @@ class DistributedStencilSolver:
         self._ph("POST_RESID")
 
     def cycle(self, m_limit: int):
+        """One restart cycle.  With device collectives (NCCL) the whole cycle —
+        phase kernels, halo exchanges and allreduces — is captured once per
+        m_limit into a CUDA graph (after one eager cycle has initialised every
+        kernel and communicator) and replayed, so the host issues one launch
+        per cycle instead of ~16 calls per Arnoldi step."""
+        if self.use_graph:
+            g = self._graphs.get(m_limit)
+            if g is None and self._eager_cycles.get(m_limit, 0) >= 1:
+                g = self._capture(m_limit)
+            if g is not None:
+                g.replay()
+                return self.state.read()
+            self._eager_cycles[m_limit] = self._eager_cycles.get(m_limit, 0) + 1
+        self._enqueue_cycle(m_limit)
+        return self.state.read()
+
+    def _capture(self, m_limit: int):
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._enqueue_cycle(m_limit)
+            torch.cuda.synchronize()
+        except Exception as exc:  # pragma: no cover - depends on the backend's capture support
+            import warnings
+            warnings.warn(f"distributed cycle capture failed ({exc}); running eagerly", stacklevel=2)
+            self.use_graph = False
+            torch.cuda.synchronize()
+            return None
+        self._graphs[m_limit] = g
+        return g
+
+    def _enqueue_cycle(self, m_limit: int) -> None:
         self._ph("START", 0, m_limit)
         self.coll.allreduce_(self.red[:2])
         self._ph("POST_START", 0, m_limit)
@@ -293,7 +343,6 @@ class DistributedStencilSolver:
             self._ph("SCALE", j, m_limit)
         self._ph("FINISH", 0, m_limit)
         self._residual()
-        return self.state.read()
 
 
 def _dist_solve(solver: DistributedStencilSolver, criteria: StopCriteria, ir: bool,
@@ -341,12 +390,12 @@ def _dist_solve(solver: DistributedStencilSolver, criteria: StopCriteria, ir: bo
 
 
 def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
-                  b_local=None, *, timer=None) -> SolveReport:
+                  b_local=None, *, timer=None, use_graph: bool = True) -> SolveReport:
     """Row-partitioned GMRES-IR (solvers.py:297-384); x returned as this
     rank's owned block (device tensor)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "ir", criteria.m, criteria.rtol, collectives,
-                                 b_local=b_local)
+                                 b_local=b_local, use_graph=use_graph)
     try:
         return _dist_solve(s, criteria, True, timer)
     finally:
@@ -354,11 +403,12 @@ def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria 
 
 
 def dist_gmres_restarted(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
-                         precision: Precision = FP64, b_local=None, *, timer=None) -> SolveReport:
+                         precision: Precision = FP64, b_local=None, *, timer=None,
+                         use_graph: bool = True) -> SolveReport:
     """Row-partitioned GMRES(m) in one precision (solvers.py:251-294)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "restarted", criteria.m, criteria.rtol, collectives,
-                                 precision=precision, b_local=b_local)
+                                 precision=precision, b_local=b_local, use_graph=use_graph)
     try:
         return _dist_solve(s, criteria, False, timer)
     finally:

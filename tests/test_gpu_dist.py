@@ -106,3 +106,50 @@ def test_ranks_sharing_one_gpu_match_single_gpu(world, kind, nx, mode):
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-8
     nr, _ = P.explicit_residual(A, b, torch.from_numpy(x).cuda())
     assert nr / float(torch.linalg.norm(b)) <= 1e-10
+
+
+def _nccl_world1(out, kind, nx, mode, use_graph):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        from paper_2109_01232_b200.dist import Collectives
+        spec = P.StencilSpec(P.StencilKind(kind), nx)
+        part = RowPartition.for_stencil(3, nx, 1, 0)
+        crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=3000)
+        coll = Collectives()
+        assert coll.capturable
+        f = dist_gmres_ir if mode == "ir" else dist_gmres_restarted
+        import warnings
+        with warnings.catch_warnings():
+            warnings.simplefilter("error")        # a failed capture would fall back with a warning
+            rep = f(spec, part, coll, crit, use_graph=use_graph)
+        out.put((rep.total_iters, rep.converged, [tuple(e) for e in rep.residual_history], rep.x.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["ir", "fp64"])
+def test_nccl_world1_graph_captured_cycle_bitwise_equals_fused(mode):
+    """The multi-GPU production path (NCCL collectives, whole cycles captured
+    into CUDA graphs with the halo/allreduce calls inside) at world size 1:
+    bit-identical to the fused single-GPU solve, eager and graph-replayed."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    kind, nx = "laplace3d", 22
+    A = P.generate(P.StencilSpec(P.StencilKind(kind), nx))
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=3000)
+    ref = P.gmres_ir(A, b, criteria=crit) if mode == "ir" else P.gmres_restarted(A, b, criteria=crit)
+    for use_graph in (True, False):
+        q = ctx.Queue()
+        p = ctx.Process(target=_nccl_world1, args=(q, kind, nx, mode, use_graph))
+        p.start()
+        iters, conv, hist, x = q.get(timeout=300)
+        p.join(timeout=60)
+        assert p.exitcode == 0
+        assert iters == ref.total_iters and conv == ref.converged
+        assert np.array_equal(x, ref.x.cpu().numpy())
+        assert hist == [tuple(e) for e in ref.residual_history]
