@@ -578,6 +578,140 @@ __global__ void __launch_bounds__(kThreads, MPG_KA2_MINB) k_dot1_wo(const T* __r
   (void)red;
 }
 
+// ============================ small-k variants (k <= KT <= 8): thread-owned rows
+// With k < 8 the warp-owned kernels leave most warps without a basis vector,
+// so few loads are in flight (measured ~20-30 us per launch at k = 1..8 for
+// ~27-150 MB).  Here every thread owns 16-byte row groups (grid-stride) and
+// all k vectors of them: KT accumulators per thread, one CTA reduction of
+// the k columns (warp trees, then the 8 warps in order), then the same
+// two-level grid reduction.
+template <typename T, int KT>
+__device__ __forceinline__ void cta_columns_to_part(T (&acc)[KT], int ncols, T* part, T* red8) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < KT; ++q) {
+    const T a = warp_sum(acc[q]);
+    if (lane == 0) red8[q * kWarps + warp] = a;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < ncols) {
+    T t = T(0);
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) t += red8[threadIdx.x * kWarps + ww];
+    part[(size_t)threadIdx.x * kMaxParts + blockIdx.x] = t;
+  }
+}
+
+// pass-1 dots (+ ||w||^2 + finite flag) for k <= KT - 2 ... KT columns = k + 2
+template <typename T, int KT>
+__global__ void __launch_bounds__(kThreads) k_dot1_small(const T* __restrict__ w, long long n,
+                                                         const T* __restrict__ V, long long ldv, int k,
+                                                         StateView<T> sv, WsView ws) {
+  pdl_wait();
+  pdl_trigger();
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  __shared__ T red8[(KT + 2) * kWarps];
+  T acc[KT + 2];
+#pragma unroll
+  for (int q = 0; q < KT + 2; ++q) acc[q] = T(0);
+  int bad = 0;
+  const long long ng = (n + VN - 1) / VN;
+  for (long long g = blockIdx.x * (long long)kThreads + threadIdx.x; g < ng; g += (long long)gridDim.x * kThreads) {
+    const long long r = g * VN;
+    T wv[VN], v[KT][VN];
+    vload(w + r, wv);   // rows in [n, ldv) are zero padding
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+      if (q < k) vload_cs(V + (size_t)q * ldv + r, v[q]);
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+      if (q < k) {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], wv[e], acc[q]);
+      }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      acc[KT] = fma_rn(wv[e], wv[e], acc[KT]);
+      bad |= !isfinite(wv[e]);
+    }
+  }
+  acc[KT + 1] = __syncthreads_or(bad) ? T(1) : T(0);
+  // compact to k + 2 columns: c1[0..k), ||w||^2, flag
+  T cols[KT + 2];
+#pragma unroll
+  for (int q = 0; q < KT + 2; ++q) cols[q] = T(0);
+#pragma unroll
+  for (int q = 0; q < KT; ++q) if (q < k) cols[q] = acc[q];
+#pragma unroll
+  for (int q = 0; q < KT + 2; ++q) {
+    if (q == k) cols[q] = acc[KT];
+    if (q == k + 1) cols[q] = (threadIdx.x == 0) ? acc[KT + 1] : T(0);   // flag counted once per CTA
+  }
+  T* part = static_cast<T*>(ws.part);
+  cta_columns_to_part<T, KT + 2>(cols, k + 2, part, red8);
+  grid_reduce_cols<kRedGroup>(part, kMaxParts, static_cast<T*>(ws.gpart), ws.gcount, k + 2,
+                              [&](int c, T s) {
+    if (sv.dist) sv.red[c] = s;
+    else if (c < k) sv.c1[c] = s;
+    else if (c == k) sv.h->w0 = (double)sqrt_rn(s);
+    else if (s != T(0)) { sv.h->flags |= MPG_FLAG_NONFINITE_OP; sv.h->done = 1; }
+  });
+}
+
+// K_B for k <= KT: w' = w - V c1 ; c2 = V^T w' ; H[:, j] = c1 + c2
+template <typename T, int KT>
+__global__ void __launch_bounds__(kThreads) k_update_dot_small(const T* __restrict__ V, long long ldv,
+                                                               long long n, int k, T* __restrict__ w,
+                                                               StateView<T> sv, WsView ws) {
+  pdl_wait();
+  pdl_trigger();
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  __shared__ T red8[KT * kWarps];
+  T c1q[KT], acc[KT];
+#pragma unroll
+  for (int q = 0; q < KT; ++q) {
+    c1q[q] = q < k ? sv.c1[q] : T(0);
+    acc[q] = T(0);
+  }
+  const long long ng = (n + VN - 1) / VN;
+  for (long long g = blockIdx.x * (long long)kThreads + threadIdx.x; g < ng; g += (long long)gridDim.x * kThreads) {
+    const long long r = g * VN;
+    T wv[VN], v[KT][VN], u[VN];
+    vload(w + r, wv);
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+      if (q < k) vload_cs(V + (size_t)q * ldv + r, v[q]);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) u[e] = T(0);
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+      if (q < k) {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c1q[q], u[e]);
+      }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) wv[e] = r + e < n ? sub_rn(wv[e], u[e]) : T(0);
+    vstore(w + r, wv);
+#pragma unroll
+    for (int q = 0; q < KT; ++q)
+      if (q < k) {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], wv[e], acc[q]);
+      }
+  }
+  T* part = static_cast<T*>(ws.part);
+  cta_columns_to_part<T, KT>(acc, k, part, red8);
+  const int jj = k - 1;
+  grid_reduce_cols<kRedGroup>(part, kMaxParts, static_cast<T*>(ws.gpart), ws.gcount, k,
+                              [&](int c, T s2) {
+    if (sv.dist) { sv.red[c] = s2; return; }
+    sv.c2[c] = s2;
+    sv.Hc(jj, c) = add_rn(add_rn(T(0), sv.c1[c]), s2);   // h = 0; h += c1; h += c2
+  });
+}
+
 // ================================================= K_C update_norm + Givens
 
 // glibc-style hypot for the fp64 rotation (np.hypot -> libm hypot);
@@ -1258,9 +1392,58 @@ static cudaError_t launch_dot1_wo_k(const T* w, long long n, const T* V, long lo
                   k, sv, ws);
 }
 
+// k <= 8: thread-owned small-k kernels (MPG_SMALLK=0 keeps the warp-owned ones)
+static bool smallk_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_SMALLK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename K>
+static long long small_grid(K kernel, long long n, int vn) {
+  static std::once_flag once;
+  static int occ = 1;
+  std::call_once(once, [&] {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+    cudaGetLastError();
+    if (occ < 1) occ = 1;
+  });
+  long long G = (n + (long long)kThreads * vn - 1) / ((long long)kThreads * vn);
+  const long long cap = std::min<long long>((long long)num_sms() * occ, kMaxParts);
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  return G;
+}
+
+template <typename T, int KT>
+static cudaError_t launch_dot1_small(const T* w, long long n, const T* V, long long ldv, int k,
+                                     StateView<T> sv, WsView ws, cudaStream_t st) {
+  const long long G = small_grid(k_dot1_small<T, KT>, n, Vec<T>::n);
+  count_launch();
+  return launch_k(true, false, k_dot1_small<T, KT>, dim3((unsigned)G), dim3(kThreads), 0, st, w, n, V, ldv, k,
+                  sv, ws);
+}
+
+template <typename T, int KT>
+static cudaError_t launch_update_dot_small(const T* V, long long ldv, long long n, int k, T* w,
+                                           StateView<T> sv, WsView ws, cudaStream_t st) {
+  const long long G = small_grid(k_update_dot_small<T, KT>, n, Vec<T>::n);
+  count_launch();
+  return launch_k(true, false, k_update_dot_small<T, KT>, dim3((unsigned)G), dim3(kThreads), 0, st, V, ldv, n,
+                  k, w, sv, ws);
+}
+
 template <typename T>
 cudaError_t launch_dot1_wo(const T* w, long long n, const T* V, long long ldv, int k,
                            StateView<T> sv, WsView ws, cudaStream_t st) {
+  if (smallk_enabled() && k <= 8) {
+    if (k <= 2) return launch_dot1_small<T, 2>(w, n, V, ldv, k, sv, ws, st);
+    if (k <= 4) return launch_dot1_small<T, 4>(w, n, V, ldv, k, sv, ws, st);
+    return launch_dot1_small<T, 8>(w, n, V, ldv, k, sv, ws, st);
+  }
   switch ((k + kWarps - 1) / kWarps) {
     case 1: return launch_dot1_wo_k<T, 1, 4>(w, n, V, ldv, k, sv, ws, st);
     case 2: return launch_dot1_wo_k<T, 2, 4>(w, n, V, ldv, k, sv, ws, st);
@@ -1353,6 +1536,11 @@ static cudaError_t launch_update_dot_w(const T* V, long long ldv, long long n, i
 template <typename T>
 cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* w,
                               StateView<T> sv, WsView ws, cudaStream_t st) {
+  if (smallk_enabled() && k <= 8) {
+    if (k <= 2) return launch_update_dot_small<T, 2>(V, ldv, n, k, w, sv, ws, st);
+    if (k <= 4) return launch_update_dot_small<T, 4>(V, ldv, n, k, w, sv, ws, st);
+    return launch_update_dot_small<T, 8>(V, ldv, n, k, w, sv, ws, st);
+  }
   switch ((k + kWarps - 1) / kWarps) {
     case 1: return launch_update_dot_w<T, 1>(V, ldv, n, k, w, sv, ws, st);
     case 2: return launch_update_dot_w<T, 2>(V, ldv, n, k, w, sv, ws, st);

@@ -313,9 +313,13 @@ def test_cfg2_laplace3d150_full_solve_vs_reference(solver, cfg2_reference):
     rep = P.gmres_ir(A, b, criteria=crit) if solver == "ir" else P.gmres_restarted(A, b, criteria=crit)
     assert rep.converged
     assert iters_match(rep, g, 50), (rep.total_iters, g["total_iters"])
+    # residual trajectory: within 2x of the reference at every restart boundary
+    # while it is well above the tolerance; in the last cycles the per-cycle
+    # reduction swings with the summation order (e.g. cfg3 IR: 6.1e-10 ->
+    # 3.5e-10 -> 8.2e-11), so there only the count rule above applies
     ours = {e.iteration: e.explicit for e in rep.residual_history if e.explicit is not None}
     for it, _, ref_exp, _ in g["boundaries"]:
-        if it in ours and it > 0:
+        if it in ours and it > 0 and ref_exp > 100 * 1e-10:
             assert 0.5 <= ours[it] / ref_exp <= 2.0, (it, ours[it], ref_exp)
     nr, _ = P.explicit_residual(A, b, rep.x)
     assert nr / float(torch.linalg.norm(b)) <= 1e-10
@@ -350,9 +354,13 @@ def test_cfg3_convdiff1500_full_solve_vs_reference(solver, cfg3_reference):
         rep = P.gmres_ir(A, b, criteria=crit, precond_fp32=M)
     assert rep.converged
     assert iters_match(rep, g, 50), (rep.total_iters, g["total_iters"], g["boundaries"][-3:])
+    # residual trajectory: within 2x of the reference at every restart boundary
+    # while it is well above the tolerance; in the last cycles the per-cycle
+    # reduction swings with the summation order (e.g. cfg3 IR: 6.1e-10 ->
+    # 3.5e-10 -> 8.2e-11), so there only the count rule above applies
     ours = {e.iteration: e.explicit for e in rep.residual_history if e.explicit is not None}
     for it, _, ref_exp, _ in g["boundaries"]:
-        if it in ours and it > 0:
+        if it in ours and it > 0 and ref_exp > 100 * 1e-10:
             assert 0.5 <= ours[it] / ref_exp <= 2.0, (it, ours[it], ref_exp)
     nr, _ = P.explicit_residual(A, b, rep.x)
     assert nr / float(torch.linalg.norm(b)) <= 1e-10
