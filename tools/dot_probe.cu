@@ -5,6 +5,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dot_probe tools/dot_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #include "../paper_2109_01232_b200/csrc/common.cuh"
 
@@ -118,6 +120,22 @@ __global__ void __launch_bounds__(256, MINB) k_dot_fin(const float* __restrict__
     if (lane == 0 && warp + 8 * q < k) part[(size_t)blockIdx.x * stride + warp + 8 * q] = a;
   }
   if (!FIN) return;
+  if (FIN == 3) {   // cluster of 8: DSMEM reduction, one partial per cluster, no grid finalize
+    __shared__ float cs[80];
+    cg::cluster_group cl = cg::this_cluster();
+    __syncthreads();
+    for (int c = threadIdx.x; c < stride; c += blockDim.x) cs[c] = part[(size_t)blockIdx.x * stride + c];
+    cl.sync();
+    if (cl.block_rank() == 0) {
+      for (int c = threadIdx.x; c < stride; c += blockDim.x) {
+        float t = 0.f;
+        for (int r = 0; r < 8; ++r) t += cl.map_shared_rank(cs, r)[c];
+        out[(size_t)(blockIdx.x / 8) * stride + c] = t;
+      }
+    }
+    cl.sync();
+    return;
+  }
   if (FIN == 2) {
     extern __shared__ float dummy[];
     (void)dummy;
@@ -180,9 +198,26 @@ template <int KV, int U, int MINB, int FIN>
 void run_fin(const float* w, long long n, const float* V, long long ldv, int k, float* part, float* out, int sms) {
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dot_fin<KV, U, MINB, FIN>, 256, 0);
-  const int G = sms * occ;
-  float t = time_it([&] { k_dot_fin<KV, U, MINB, FIN><<<G, 256>>>(w, n, V, ldv, k, part, out); });
-  printf("warp-owned+partials KV=%d U=%d minb=%d fin=%d: occ %d  %7.0f GB/s  %.1f us\n", KV, U, MINB, FIN, occ,
+  int G = sms * occ;
+  float t;
+  if (FIN == 3) {
+    G = G / 8 * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G); cfg.blockDim = dim3(256); cfg.stream = 0;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 8; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at; cfg.numAttrs = 1;
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, k_dot_fin<KV, U, MINB, FIN>, &cfg);
+    if (ncl * 8 < G) G = ncl * 8;
+    cfg.gridDim = dim3(G);
+    t = time_it([&] { cudaLaunchKernelEx(&cfg, k_dot_fin<KV, U, MINB, FIN>, w, n, V, ldv, k, part, out); });
+  } else {
+    t = time_it([&] { k_dot_fin<KV, U, MINB, FIN><<<G, 256>>>(w, n, V, ldv, k, part, out); });
+  }
+  occ = G;
+  printf("warp-owned+partials KV=%d U=%d minb=%d fin=%d: grid %d  %7.0f GB/s  %.1f us\n", KV, U, MINB, FIN, occ,
          (double)(k + 1) * n * 4 / t / 1e6, t * 1e3);
 }
 
@@ -214,6 +249,9 @@ int main() {
   run_fin<4, 1, 6, 1>(w, n, V, ldv, k, part, outv, sms);
   run_fin<4, 2, 1, 2>(w, n, V, ldv, k, part, outv, sms);
   run_fin<4, 1, 6, 2>(w, n, V, ldv, k, part, outv, sms);
+  run_fin<4, 2, 4, 0>(w, n, V, ldv, k, part, outv, sms);
+  run_fin<4, 2, 4, 3>(w, n, V, ldv, k, part, outv, sms);
+  run_fin<4, 1, 6, 3>(w, n, V, ldv, k, part, outv, sms);
   run_rows<32, 1>(w, n, V, ldv, k, out, sms);
   run_rows<32, 2>(w, n, V, ldv, k, out, sms);
   run_rows<32, 3>(w, n, V, ldv, k, out, sms);
