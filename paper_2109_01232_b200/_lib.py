@@ -103,8 +103,9 @@ _SIGS = {
     "mpg_solver_profile_cycle": (C.c_int, [_vp, _i32, _vp, C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
 }
 PROFILE_CLASSES = ("start", "precond", "spmv_dot1", "update_dot", "update_norm_givens",
-                   "scale", "finish", "residual", "dot1")
-# with K_A split (the default) "spmv_dot1" times the SpMV alone and "dot1" the pass-1 dots
+                   "scale", "finish", "residual", "dot1", "step")
+# with K_A split "spmv_dot1" times the SpMV alone and "dot1" the pass-1 dots; "step" is the
+# persistent per-step kernel (stencil storage, no preconditioner; MPG_MEGA=0 disables it)
 
 _LIB = None
 _ERR: str | None = None

@@ -12,14 +12,12 @@
 #include <cstdlib>
 #include <mutex>
 
+#include "arnoldi_common.cuh"
 #include "spmv.cuh"
 #include "state.cuh"
 
 namespace mpg {
 
-__device__ __forceinline__ bool gated(const mpg_state_header* h) {
-  return *(volatile const int*)&h->done != 0;
-}
 
 // ============================================================== K_B update_dot
 // TMA-staged: a producer warp bulk-copies the tile slices V[0..k)[tile] and
@@ -714,86 +712,6 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_small(const T* __restri
 
 // ================================================= K_C update_norm + Givens
 
-// glibc-style hypot for the fp64 rotation (np.hypot -> libm hypot);
-// fp32 follows glibc hypotf: correctly rounded double evaluation.
-__device__ __forceinline__ float hypot_ref(float a, float b) {
-  const double x = (double)a, y = (double)b;
-  return (float)__dsqrt_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
-}
-__device__ double hypot_kernel(double ax, double ay) {
-  // ax >= ay > 0, both well inside the exponent range (Borges 2019, as glibc)
-  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
-  double t1, t2;
-  if (h <= 2.0 * ay) {
-    const double delta = h - ay;
-    t1 = ax * (2.0 * delta - ax);
-    t2 = (delta - 2.0 * (ax - ay)) * delta;
-  } else {
-    const double delta = h - ax;
-    t1 = 2.0 * delta * (ax - 2.0 * ay);
-    t2 = (4.0 * delta - ay) * ay + delta * delta;
-  }
-  h -= (t1 + t2) / (2.0 * h);
-  return h;
-}
-__device__ __forceinline__ double hypot_ref(double a, double b) {
-  double ax = fabs(a), ay = fabs(b);
-  if (isinf(ax) || isinf(ay)) return __longlong_as_double(0x7ff0000000000000LL);
-  if (isnan(ax) || isnan(ay)) return ax + ay;
-  if (ax < ay) { const double t = ax; ax = ay; ay = t; }
-  if (ay == 0.0) return ax;
-  if (ax > 0x1p+511) {
-    if (ay <= ax * 0x1p-54) return ax + ay;
-    return hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) * 0x1p+600;
-  }
-  if (ay < 0x1p-511) {
-    if (ax >= ay * 0x1p+54) return ax + ay;
-    return hypot_kernel(ax * 0x1p+600, ay * 0x1p+600) * 0x1p-600;
-  }
-  if (ay <= ax * 0x1p-54) return ax + ay;
-  return hypot_kernel(ax, ay);
-}
-
-// Rotate column j into the triangular factor (krylov.py:154-187).  One thread.
-template <typename T>
-__device__ void givens_column(const StateView<T>& sv, int j, double threshold, bool brk,
-                              int m_limit) {
-  T* col = &sv.Rc(j, 0);
-  for (int i = 0; i <= j + 1; ++i) col[i] = sv.Hc(j, i);
-  for (int i = 0; i < j; ++i) {
-    const T c = sv.cs[i], s = sv.sn[i];
-    const T a = col[i], b = col[i + 1];
-    const T top = add_rn(mul_rn(c, a), mul_rn(s, b));
-    col[i + 1] = add_rn(mul_rn(-s, a), mul_rn(c, b));
-    col[i] = top;
-  }
-  const T a = col[j], b = col[j + 1];
-  const T r = hypot_ref(a, b);
-  double res;
-  if (r == T(0)) {
-    sv.cs[j] = T(1);
-    sv.sn[j] = T(0);
-    res = (double)fabs(sv.g[j]);
-  } else {
-    const T c = div_rn(a, r), s = div_rn(b, r);
-    sv.cs[j] = c;
-    sv.sn[j] = s;
-    col[j] = add_rn(mul_rn(c, a), mul_rn(s, b));
-    col[j + 1] = T(0);
-    const T gj = sv.g[j], gj1 = sv.g[j + 1];
-    const T top = add_rn(mul_rn(c, gj), mul_rn(s, gj1));
-    sv.g[j + 1] = add_rn(mul_rn(-s, gj), mul_rn(c, gj1));
-    sv.g[j] = top;
-    res = (double)fabs(sv.g[j + 1]);
-  }
-  sv.implicit[j] = res;
-  sv.h->steps = j + 1;
-  sv.h->breakdown = brk ? 1 : 0;
-  // solvers.py:160-168: stop on breakdown, on the implicit threshold, or when
-  // the cycle's step budget is exhausted
-  if (brk || res <= threshold || j + 1 >= m_limit) sv.h->done = 1;
-}
-
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ V, long long ldv,
                                                           long long n, int j, T* __restrict__ w,
@@ -896,28 +814,6 @@ __global__ void __launch_bounds__(kThreads) k_step_scale(const T* __restrict__ w
 // This drops K_S's launch and its 2 n s bytes (read w, write v) for n s (write v).
 // Shared arrival counter + generation word in the workspace; the last arriver
 // resets the counter before releasing, so the slot is reusable.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned g0 = ld_acquire_u32(gen);
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (ld_acquire_u32(gen) == g0) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 template <typename T, bool CACHE>
 __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(const T* __restrict__ V, long long ldv,
                                                                 long long n, int j, T* __restrict__ w,

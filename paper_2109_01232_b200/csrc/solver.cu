@@ -44,7 +44,8 @@ struct ProfScope {
   }
 };
 enum { PK_START = 0, PK_PRECOND, PK_SPMV_DOT, PK_UPDATE_DOT, PK_UPDATE_NORM, PK_SCALE, PK_FINISH,
-       PK_RESIDUAL, PK_DOT1, PK_COUNT };   // PK_SPMV_DOT: the SpMV alone when K_A is split
+       PK_RESIDUAL, PK_DOT1, PK_STEP, PK_COUNT };   // PK_SPMV_DOT: the SpMV alone when K_A is split;
+                                                    // PK_STEP: the persistent per-step kernel
 
 #define TRY(...)                       \
   do {                                   \
@@ -236,8 +237,21 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   // 10 us scaling launch saves, so the fused variant stays off (kept for A/B runs).
   const bool fuse = false && d.pc_kind == MPG_PC_NONE && d.m <= 64;
   T* wbuf[2] = {w, fuse ? static_cast<T*>(d.u) : w};
+  // single-GPU stencil storage without a preconditioner: one persistent
+  // cooperative kernel per Arnoldi step (step_kernel.cu) when it applies
+  const bool mega = mega_enabled() && !fuse && d.pc_kind == MPG_PC_NONE && !d.dist && d.stencil_dims &&
+                    d.dia && d.halo >= (d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx
+                                                            : (long long)d.stencil_nx);
   for (int j = 0; j < m_limit; ++j) {
     T* wj = wbuf[j & 1];
+    if (mega && j + 3 <= 72) {
+      ProfScope ps(PK_STEP);
+      StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
+                       d.stencil_dims, d.row0};
+      S.padded = 1;
+      TRY(launch_step_mega<T>(S, V + (size_t)j * d.ldv, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st));
+      continue;
+    }
     if (fuse && j > 0) {
       ProfScope ps(PK_SPMV_DOT);
       const T* hprev = sv.H + (size_t)(j - 1) * (d.m + 1) + j;   // H[j, j-1] = h_sub of step j-1

@@ -339,18 +339,68 @@ __device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)
 // also feeds the +-1 neighbours (plus one scalar each), and one window load
 // per +-nx / +-nx^2 neighbour (16-byte when aligned).  The per-row reduction is
 // stencil_row_padded's: add.reduceat order over the present slots, bit-exact.
+// One 16-byte group of VN consecutive rows r0.. (r0 % VN == 0) on padded
+// inputs: S 16-byte value loads (slot-major storage is VN-aligned), one 16-byte
+// load of x[r0..] that also feeds the +-1 neighbours (plus one scalar each),
+// one window load per +-nx / +-nx^2 neighbour (16-byte when aligned).  The
+// per-row reduction is stencil_row_padded's: add.reduceat order over the
+// present slots, bit-exact.  mis[s] = (off[s] mod VN).
+template <typename T, int S>
+__device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
+                                              long long r0, const long long (&off)[S],
+                                              const int (&mis)[S], T (&y)[Vec<T>::n]) {
+  constexpr int VN = Vec<T>::n;
+  constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
+  const size_t ld = (size_t)SV.ldv;
+  T pv[S][VN], px[S][VN];
+#pragma unroll
+  for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
+  vload(x + r0, px[C]);
+  const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (s < C - 1 || s > C + 1) xwindow(x + r0 + off[s], mis[s], px[s]);
+  px[C - 1][0] = xm;
+#pragma unroll
+  for (int e = 1; e < VN; ++e) px[C - 1][e] = px[C][e - 1];
+#pragma unroll
+  for (int e = 0; e < VN - 1; ++e) px[C + 1][e] = px[C][e + 1];
+  px[C + 1][VN - 1] = xp;
+#pragma unroll
+  for (int e = 0; e < VN; ++e) {
+    bool have = false;
+    T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const T p = mul_rn(pv[s][e], px[s][e]);
+      const bool pr = present(pv[s][e]);
+      const T nrest = add_rn(rest, p);
+      rest = (pr && have) ? nrest : rest;
+      p0 = (pr && !have) ? p : p0;
+      have = have || pr;
+    }
+    y[e] = add_rn(p0, rest);
+  }
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void stencil_mis(const long long (&off)[S], int (&mis)[S]) {
+  constexpr int VN = Vec<T>::n;
+#pragma unroll
+  for (int s = 0; s < S; ++s) mis[s] = (int)(((off[s] % VN) + VN) % VN);
+}
+
+// Vectorised branchless stencil rows on padded inputs: each consumer thread
+// owns one 16-byte group of VN consecutive rows per tile (stencil_group).
 template <typename T, int S, typename E>
 __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const T* __restrict__ x,
                                                  const long long (&off)[S], E& epi,
                                                  EpiShared<T>& es) {
   constexpr int VN = Vec<T>::n;
   constexpr int TILE = kSpConsumers * VN;
-  constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
   const long long n = SV.n;
-  const size_t ld = (size_t)SV.ldv;
   int mis[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) mis[s] = (int)(((off[s] % VN) + VN) % VN);
+  stencil_mis<T, S>(off, mis);
   const long long ntiles = (n + TILE - 1) / TILE;
   int t = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
@@ -360,36 +410,8 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
     const int rr = threadIdx.x * VN;
     if (rr < nrows) {
       const long long r0 = a + rr;
-      T pv[S][VN], px[S][VN];
-#pragma unroll
-      for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
-      vload(x + r0, px[C]);
-      const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
-#pragma unroll
-      for (int s = 0; s < S; ++s)
-        if (s < C - 1 || s > C + 1) xwindow(x + r0 + off[s], mis[s], px[s]);
-      px[C - 1][0] = xm;
-#pragma unroll
-      for (int e = 1; e < VN; ++e) px[C - 1][e] = px[C][e - 1];
-#pragma unroll
-      for (int e = 0; e < VN - 1; ++e) px[C + 1][e] = px[C][e + 1];
-      px[C + 1][VN - 1] = xp;
       T y[VN];
-#pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        bool have = false;
-        T p0 = T(0), rest = T(-0.0);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-          const T p = mul_rn(pv[s][e], px[s][e]);
-          const bool pr = present(pv[s][e]);
-          const T nrest = add_rn(rest, p);
-          rest = (pr && have) ? nrest : rest;
-          p0 = (pr && !have) ? p : p0;
-          have = have || pr;
-        }
-        y[e] = add_rn(p0, rest);
-      }
+      stencil_group<T, S>(SV, x, r0, off, mis, y);
       epi_rows(epi, r0, y, min(VN, nrows - rr), ys + rr);
     }
     consumer_sync();

@@ -153,6 +153,12 @@ cudaError_t launch_start_scale(const T* r0, T* v0, long long n, StateView<T> sv,
 template <typename T>
 cudaError_t launch_lsq(StateView<T> sv, cudaStream_t st);
 
+// persistent per-step kernel (step_kernel.cu), stencil storage, single GPU
+template <typename T>
+cudaError_t launch_step_mega(const StencilView<T>& S, const T* x, T* V, long long ldv, long long n, int j,
+                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st);
+bool mega_enabled();   // MPG_MEGA=0 selects the four-launch step
+
 // distributed-mode post phases (k_dist_post)
 enum DistPostPhase {
   DP_POST_START = 0,

@@ -1,0 +1,442 @@
+// Persistent per-step Arnoldi kernel for stencil storage (single GPU).
+//
+// One cooperative launch runs a whole CGS2 Arnoldi step (krylov.py:112-151 +
+// givens_update :154-187) on 148 CTAs of 1024 threads (one per SM).  Each CTA
+// owns a fixed set of 32*VN-row blocks (dealt round-robin over the grid) for
+// every phase, so the new vector w = A v_j never leaves shared memory:
+//
+//   P1   w = A v_j for the CTA's rows (stencil_group, bit-exact SpMV);
+//        ||w||^2 and the finite flag; w kept in shared memory
+//   P1b  pass-1 dots c1 = V^T w: four row groups of 8 warps, warp owns
+//        basis vectors gw + 8q (16-byte lane slices, KV accumulators)
+//   B1   grid barrier; every CTA sums the 148 CTA partials of each column in
+//        the same fixed order (warp per column) -> c1, w0, flag
+//   P2   w' = w - V c1 (8 warp partials of u summed per row in warp order
+//        through shared memory) and pass-2 dots c2 = V^T w' from the same
+//        registers: the basis is read once for both halves
+//   B2   grid barrier; c2; CTA 0 writes c1, c2 and the Hessenberg column
+//   P3   w'' = w' - V c2, ||w''||^2
+//   B3   grid barrier; h_sub; breakdown test; CTA 0 rotates the column
+//        (givens_column) and sets the done flag
+//   P4   V[:, j+1] = w'' / h_sub for the CTA's rows (IEEE division)
+//
+// Against the four-launch step (K_A1, K_A2, K_B, K_CS) this removes three
+// kernel boundaries and their reduction tails, and w's global write and its
+// three re-reads.  When a CTA's rows do not fit in shared memory (n >~ 13M
+// rows fp32 / 6.5M fp64) the CACHE = false variant keeps w in global memory.
+// The basis is swept three times per step, as in the four-launch path.
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
+#include "arnoldi_common.cuh"
+#include "spmv.cuh"
+#include "state.cuh"
+
+namespace mpg {
+
+constexpr int kMegaThreads = 1024;
+constexpr int kMegaWarps = kMegaThreads / 32;
+constexpr int kMegaGroups = kMegaWarps / 8;   // row groups of 8 warps
+constexpr int kMegaMaxCols = 72;              // k + 2 <= kMegaMaxCols (m <= 64)
+// column blocks of the (column-major) partial array, one per barrier, so a fast
+// CTA never overwrites partials a slow CTA is still summing
+constexpr int kColDot1 = 0;
+constexpr int kColDot2 = kMegaMaxCols;
+constexpr int kColNorm = 2 * kMegaMaxCols;
+
+__device__ __forceinline__ void group_sync(int grp) {
+  asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
+}
+
+// Sum column `col` of the CTA partials in a fixed order (warp-level), all lanes get it.
+template <typename T>
+__device__ __forceinline__ T sum_column(const T* part, int col, int G) {
+  const int lane = threadIdx.x & 31;
+  T s = T(0);
+  for (int p = lane; p < G; p += 32) s += __ldcg(part + (size_t)col * kMaxParts + p);
+  return warp_sum(s);
+}
+
+template <typename T, int S, int KV, bool CACHE>
+__global__ void __launch_bounds__(kMegaThreads, 1)
+k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
+            T* wg, StateView<T> sv, WsView ws, int m_limit) {
+  if (gated(sv.h)) return;
+  constexpr int VN = Vec<T>::n;
+  constexpr int RB = 32 * VN;
+  constexpr int RPW = RB / 8;
+  const int k = j + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int grp = warp >> 3, gw = warp & 7;
+  const int G = gridDim.x;
+  const long long nblk = (n + RB - 1) / RB;
+  const int nb = (long long)blockIdx.x < nblk ? (int)((nblk - 1 - blockIdx.x) / G + 1) : 0;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* wsm = reinterpret_cast<T*>(smraw);
+  __shared__ __align__(16) T upart[kMegaGroups][8][RB];
+  __shared__ __align__(16) T xs[kMegaGroups][RB];
+  __shared__ T cred[kMegaGroups][kMegaMaxCols];
+  __shared__ T c1v[kMegaMaxCols];
+  __shared__ T c2v[kMegaMaxCols];
+  __shared__ T red[kMegaWarps];
+  __shared__ int badw[kMegaWarps];
+  T* part = static_cast<T*>(ws.part);
+  auto bstart = [&](int t) -> long long { return ((long long)blockIdx.x + (long long)t * G) * RB; };
+  auto wptr = [&](int t) -> T* { return CACHE ? wsm + (size_t)t * RB : wg + bstart(t); };
+
+  // ---------------------------------------------------------------- P1 SpMV
+  long long off[S];
+  {
+    const long long nx = SV.nx, p2 = nx * nx;
+    if constexpr (S == 7) {
+      const long long o[7] = {-p2, -nx, -1, 0, 1, nx, p2};
+#pragma unroll
+      for (int s = 0; s < 7; ++s) off[s] = o[s];
+    } else {
+      const long long o[5] = {-nx, -1, 0, 1, nx};
+#pragma unroll
+      for (int s = 0; s < 5; ++s) off[s] = o[s];
+    }
+  }
+  int mis[S];
+  stencil_mis<T, S>(off, mis);
+  T ss = T(0);
+  int bad = 0;
+  for (int L = tid; L < nb * 32; L += kMegaThreads) {
+    const int t = L >> 5, l = L & 31;
+    const long long r0 = bstart(t) + (long long)l * VN;
+    T y[VN];
+    if (r0 < n) {
+      stencil_group<T, S>(SV, x, r0, off, mis, y);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) y[e] = r0 + e < n ? y[e] : T(0);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VN; ++e) y[e] = T(0);
+    }
+    if (CACHE || r0 < n) vstore(wptr(t) + l * VN, y);   // global w ends at ldv
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      ss = fma_rn(y[e], y[e], ss);
+      bad |= !isfinite(y[e]);
+    }
+  }
+  __syncthreads();
+
+  // --------------------------------------------------------- P1b c1 = V^T w
+  {
+    T acc[KV];
+#pragma unroll
+    for (int q = 0; q < KV; ++q) acc[q] = T(0);
+    for (int t = grp; t < nb; t += kMegaGroups) {
+      const long long r = bstart(t) + (long long)lane * VN;
+      const bool in = r < n;
+      T wv[VN], v[KV][VN];
+      if (CACHE || in) vload_smem(wptr(t) + lane * VN, wv);
+      else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) wv[e] = T(0);
+      }
+#pragma unroll
+      for (int q = 0; q < KV; ++q) {
+        const int i = gw + 8 * q;
+        if (in && i < k) vload_cs(V + (size_t)i * ldv + r, v[q]);
+        else {
+#pragma unroll
+          for (int e = 0; e < VN; ++e) v[q][e] = T(0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < KV; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], wv[e], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < KV; ++q) {
+      const int i = gw + 8 * q;
+      const T a = warp_sum(acc[q]);
+      if (lane == 0 && i < k) cred[grp][i] = a;
+    }
+  }
+  {
+    const T sw = warp_sum(ss);
+    const int bw = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      red[warp] = sw;
+      badw[warp] = bw;
+    }
+  }
+  __syncthreads();
+  if (tid < k) {
+    T t = T(0);
+#pragma unroll
+    for (int g = 0; g < kMegaGroups; ++g) t += cred[g][tid];
+    part[(size_t)(kColDot1 + tid) * kMaxParts + blockIdx.x] = t;
+  } else if (tid == k) {
+    T t = T(0);
+    for (int w = 0; w < kMegaWarps; ++w) t += red[w];
+    part[(size_t)(kColDot1 + k) * kMaxParts + blockIdx.x] = t;
+  } else if (tid == k + 1) {
+    int b = 0;
+    for (int w = 0; w < kMegaWarps; ++w) b |= badw[w];
+    part[(size_t)(kColDot1 + k + 1) * kMaxParts + blockIdx.x] = b ? T(1) : T(0);
+  }
+  grid_barrier(ws.counter, ws.counter + 1);                                       // B1
+  for (int c = warp; c < k + 2; c += kMegaWarps) {
+    const T s = sum_column(part, kColDot1 + c, G);
+    if (lane == 0) c1v[c] = s;
+  }
+  __syncthreads();
+  if (c1v[k + 1] != T(0)) {   // non-finite operator output (krylov.py:131-133): every CTA agrees
+    if (blockIdx.x == 0 && tid == 0) {
+      sv.h->flags |= MPG_FLAG_NONFINITE_OP;
+      sv.h->done = 1;
+    }
+    return;
+  }
+  const double w0 = (double)sqrt_rn(c1v[k]);
+  if (blockIdx.x == 0) {
+    if (tid < k) sv.c1[tid] = c1v[tid];
+    if (tid == 0) sv.h->w0 = w0;
+  }
+
+  // ------------------------------------ P2 w' = w - V c1 ; c2 = V^T w'
+  {
+    T acc[KV];
+#pragma unroll
+    for (int q = 0; q < KV; ++q) acc[q] = T(0);
+    const int rrow = gw * RPW + lane;
+    for (int t = grp; t < nb; t += kMegaGroups) {
+      const long long b0 = bstart(t);
+      const long long r = b0 + (long long)lane * VN;
+      const bool in = r < n;
+      T v[KV][VN], u[VN];
+#pragma unroll
+      for (int q = 0; q < KV; ++q) {
+        const int i = gw + 8 * q;
+        if (in && i < k) vload_cs(V + (size_t)i * ldv + r, v[q]);
+        else {
+#pragma unroll
+          for (int e = 0; e < VN; ++e) v[q][e] = T(0);
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VN; ++e) u[e] = T(0);
+#pragma unroll
+      for (int q = 0; q < KV; ++q) {
+        const int i = gw + 8 * q;
+        const T c = i < k ? c1v[i] : T(0);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c, u[e]);
+      }
+      vstore(upart[grp][gw] + lane * VN, u);
+      group_sync(grp);
+      if (lane < RPW) {
+        T s = T(0);
+#pragma unroll
+        for (int ww = 0; ww < 8; ++ww) s += upart[grp][ww][rrow];
+        T* wr = wptr(t) + rrow;
+        const bool rin = b0 + rrow < n;
+        const T xr = rin ? sub_rn(*wr, s) : T(0);
+        if (CACHE || rin) *wr = xr;
+        xs[grp][rrow] = xr;
+      }
+      group_sync(grp);
+      T xv[VN];
+      vload_smem(xs[grp] + lane * VN, xv);
+#pragma unroll
+      for (int q = 0; q < KV; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], xv[e], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < KV; ++q) {
+      const int i = gw + 8 * q;
+      const T a = warp_sum(acc[q]);
+      if (lane == 0 && i < k) cred[grp][i] = a;
+    }
+  }
+  __syncthreads();
+  if (tid < k) {
+    T t = T(0);
+#pragma unroll
+    for (int g = 0; g < kMegaGroups; ++g) t += cred[g][tid];
+    part[(size_t)(kColDot2 + tid) * kMaxParts + blockIdx.x] = t;
+  }
+  grid_barrier(ws.counter, ws.counter + 1);                                       // B2
+  for (int c = warp; c < k; c += kMegaWarps) {
+    const T s = sum_column(part, kColDot2 + c, G);
+    if (lane == 0) c2v[c] = s;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < k) {
+    sv.c2[tid] = c2v[tid];
+    sv.Hc(j, tid) = add_rn(add_rn(T(0), c1v[tid]), c2v[tid]);   // h = 0; h += c1; h += c2
+  }
+
+  // ----------------------------------------------- P3 w'' = w' - V c2, norm
+  T ss2 = T(0);
+  for (int L = tid; L < nb * 32; L += kMegaThreads) {
+    const int t = L >> 5, l = L & 31;
+    const long long r = bstart(t) + (long long)l * VN;
+    if (!CACHE && r >= n) continue;   // global w ends at ldv (nothing to add to ss2)
+    T* wp = wptr(t) + l * VN;
+    T wv[VN], u[VN];
+    vload_smem(wp, wv);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) u[e] = T(0);
+    if (r < n) {
+      int i = 0;
+      for (; i + 4 <= k; i += 4) {
+        T v0[VN], v1[VN], v2[VN], v3[VN];
+        vload_cs(V + (size_t)(i + 0) * ldv + r, v0);
+        vload_cs(V + (size_t)(i + 1) * ldv + r, v1);
+        vload_cs(V + (size_t)(i + 2) * ldv + r, v2);
+        vload_cs(V + (size_t)(i + 3) * ldv + r, v3);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+          u[e] = fma_rn(v0[e], c2v[i + 0], u[e]);
+          u[e] = fma_rn(v1[e], c2v[i + 1], u[e]);
+          u[e] = fma_rn(v2[e], c2v[i + 2], u[e]);
+          u[e] = fma_rn(v3[e], c2v[i + 3], u[e]);
+        }
+      }
+      for (; i < k; ++i) {
+        T v0[VN];
+        vload_cs(V + (size_t)i * ldv + r, v0);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) u[e] = fma_rn(v0[e], c2v[i], u[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      wv[e] = r + e < n ? sub_rn(wv[e], u[e]) : T(0);
+      ss2 = fma_rn(wv[e], wv[e], ss2);
+    }
+    vstore(wp, wv);
+  }
+  {
+    const T sw = warp_sum(ss2);
+    if (lane == 0) red[warp] = sw;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    T t = T(0);
+    for (int w = 0; w < kMegaWarps; ++w) t += red[w];
+    part[(size_t)kColNorm * kMaxParts + blockIdx.x] = t;
+  }
+  grid_barrier(ws.counter, ws.counter + 1);                                       // B3
+  if (warp == 0) {
+    const T s = sum_column(part, kColNorm, G);
+    if (lane == 0) red[0] = s;
+  }
+  __syncthreads();
+  const T hs = sqrt_rn(red[0]);
+  const bool brk = (double)hs <= sv.h->breakdown_tol * w0;   // krylov.py:146
+  if (blockIdx.x == 0 && tid == 0) {
+    sv.Hc(j, j + 1) = hs;
+    sv.h->h_sub = (double)hs;
+    givens_column(sv, j, sv.h->threshold, brk, m_limit);
+  }
+  if (brk) return;   // no new basis vector on breakdown
+
+  // ------------------------------------------------- P4 V[:, j+1] = w'' / h
+  T* vn = V + (size_t)(j + 1) * ldv;
+  for (int L = tid; L < nb * 32; L += kMegaThreads) {
+    const int t = L >> 5, l = L & 31;
+    const long long r = bstart(t) + (long long)l * VN;
+    if (r >= n) continue;
+    T a[VN];
+    vload_smem(wptr(t) + l * VN, a);
+#pragma unroll
+    for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);   // rows >= n stay 0
+    vstore(vn + r, a);
+  }
+}
+
+// ------------------------------------------------------------------ launch
+
+// Off by default (MPG_MEGA=1 enables): measured on B200 at cfg2 the persistent
+// step ties the four-launch step in fp32 (IR solve 0.501 s vs 0.503 s) and
+// loses in fp64 (1.123 s vs 0.999 s: 64-register cap at 1024 threads spills,
+// one CTA per SM); the three grid barriers cost what the launch boundaries did.
+bool mega_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_MEGA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <typename T, int S, int KV, bool CACHE>
+static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
+                                 int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
+                                 unsigned grid, size_t smem) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         optin - (int)sizeof(T) * (kMegaGroups * 9 * 32 * Vec<T>::n + 3 * kMegaMaxCols * 2) - 2048);
+    cudaGetLastError();
+  });
+  count_launch();
+  return launch_k(false, true, k_step_mega<T, S, KV, CACHE>, dim3(grid), dim3(kMegaThreads), smem, st, SV, x,
+                  V, ldv, n, j, w, sv, ws, m_limit);
+}
+
+template <typename T, int S, int KV>
+static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
+                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+  constexpr int RB = 32 * Vec<T>::n;
+  const long long nblk = (n + RB - 1) / RB;
+  const long long G = std::min<long long>(num_sms(), nblk);
+  const size_t cache = (size_t)((nblk + G - 1) / G) * RB * sizeof(T);
+  static int optin = -1;
+  if (optin < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  // static shared memory of the kernel (upart, xs, column scratch) + headroom
+  const size_t stat = sizeof(T) * (kMegaGroups * 9 * RB + 3 * kMegaMaxCols * 2) + 2048;
+  if (cache + stat <= (size_t)optin)
+    return launch_mega_k<T, S, KV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache);
+  return launch_mega_k<T, S, KV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0);
+}
+
+template <typename T>
+cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n, int j,
+                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+  const int k = j + 1;
+  if (k + 2 > kMegaMaxCols || !SV.padded || SV.xdiv) return cudaErrorInvalidValue;
+  const int kv = (k + 7) / 8;
+#define MEGA_CASE(KVV)                                                                            \
+  case KVV:                                                                                       \
+    return SV.dims == 3 ? launch_mega_kv<T, 7, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st)  \
+                        : launch_mega_kv<T, 5, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st);
+  switch (kv) {
+    MEGA_CASE(1)
+    MEGA_CASE(2)
+    MEGA_CASE(3)
+    MEGA_CASE(4)
+    MEGA_CASE(5)
+    MEGA_CASE(6)
+    MEGA_CASE(7)
+    default:
+      return cudaErrorInvalidValue;
+  }
+#undef MEGA_CASE
+}
+
+template cudaError_t launch_step_mega<float>(const StencilView<float>&, const float*, float*, long long,
+                                             long long, int, float*, StateView<float>, WsView, int,
+                                             cudaStream_t);
+template cudaError_t launch_step_mega<double>(const StencilView<double>&, const double*, double*, long long,
+                                              long long, int, double*, StateView<double>, WsView, int,
+                                              cudaStream_t);
+
+}  // namespace mpg
