@@ -334,6 +334,9 @@ template <typename T, int KV>
 #ifndef MPG_KCS_MINB
 #define MPG_KCS_MINB 1
 #endif
+#ifndef MPG_KCS_BATCH
+#define MPG_KCS_BATCH 4
+#endif
 __global__ void __launch_bounds__(kThreads, MPG_KB_MINB) k_update_dot_w(const T* __restrict__ V, long long ldv,
                                                            long long n, int k, T* __restrict__ w,
                                                            StateView<T> sv, WsView ws) {
@@ -844,19 +847,16 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
 #pragma unroll
     for (int e = 0; e < VN; ++e) u[e] = T(0);
     int i = 0;
-    for (; i + 4 <= k; i += 4) {
-      T v0[VN], v1[VN], v2[VN], v3[VN];
-      vload_cs(V + (size_t)(i + 0) * ldv + r, v0);
-      vload_cs(V + (size_t)(i + 1) * ldv + r, v1);
-      vload_cs(V + (size_t)(i + 2) * ldv + r, v2);
-      vload_cs(V + (size_t)(i + 3) * ldv + r, v3);
+    // MPG_KCS_BATCH basis loads in flight per thread; u accumulates in i order either way
+    constexpr int B = MPG_KCS_BATCH;
+    for (; i + B <= k; i += B) {
+      T vb[B][VN];
 #pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        u[e] = fma_rn(v0[e], c2s[i + 0], u[e]);
-        u[e] = fma_rn(v1[e], c2s[i + 1], u[e]);
-        u[e] = fma_rn(v2[e], c2s[i + 2], u[e]);
-        u[e] = fma_rn(v3[e], c2s[i + 3], u[e]);
-      }
+      for (int b = 0; b < B; ++b) vload_cs(V + (size_t)(i + b) * ldv + r, vb[b]);
+#pragma unroll
+      for (int e = 0; e < VN; ++e)
+#pragma unroll
+        for (int b = 0; b < B; ++b) u[e] = fma_rn(vb[b][e], c2s[i + b], u[e]);
     }
     for (; i < k; ++i) {
       T v0[VN];

@@ -120,13 +120,14 @@ def generate(spec) -> CsrMatrix:
 
 def make_rhs(spec: RhsSpec, n: int, *, on_device: bool = False):
     """fp64 right-hand side (gen.py:205-217); ``on_device`` returns a tensor."""
-    if spec.kind is RhsKind.ONES:
+    kind = RhsKind(spec.kind.value if hasattr(spec.kind, "value") else spec.kind)   # reference specs too
+    if kind is RhsKind.ONES:
         if on_device:
             return torch.ones(n, dtype=torch.float64, device=device())
         return np.ones(n, dtype=np.float64)
-    if spec.kind is RhsKind.RANDOM_UNIFORM01:
+    if kind is RhsKind.RANDOM_UNIFORM01:
         v = np.random.default_rng(spec.seed).random(n)
-    elif spec.kind is RhsKind.RANDOM_NORMAL:
+    elif kind is RhsKind.RANDOM_NORMAL:
         v = np.random.default_rng(spec.seed).standard_normal(n)
     else:
         vals = []
