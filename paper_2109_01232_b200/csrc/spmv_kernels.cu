@@ -1,6 +1,8 @@
 // SpMV-family kernels: plain SpMV, explicit residual, the fused
 // SpMV + first CGS pass (K_A), and the polynomial-preconditioner steps.
 // All share spmv_pipeline (spmv.cuh); they differ only in the epilogue.
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -8,6 +10,16 @@
 #include "state.cuh"
 
 namespace mpg {
+
+// MPG_CSR_TMA=1 selects the TMA-ring CSR kernel for every epilogue (A/B)
+static bool csr_warp_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_CSR_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 // Consumer-only last-CTA election (the producer warp has exited).
 __device__ __forceinline__ bool consumers_last_cta(unsigned int* counter, bool* flag) {
@@ -101,6 +113,7 @@ struct EpiResid {
 template <typename T>
 struct EpiDot1 {
   static constexpr bool kPdl = false;
+  static constexpr bool kNeedsTiles = true;
   T* w;
   const T* V;
   long long ldv;
@@ -171,6 +184,7 @@ struct EpiDot1 {
 template <typename T, int KV>
 struct EpiDot1Warp {
   static constexpr bool kPdl = false;
+  static constexpr bool kNeedsTiles = true;
   static constexpr int VN = 16 / (int)sizeof(T);
   static constexpr int RB = 32 * VN;
   T* w;
@@ -417,6 +431,76 @@ __global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, cons
   stencil_pipeline(S, x, epi, es);
 }
 
+// ------------------------------------------------------------------------
+// CSR SpMV, warp-chunk design (the default for epilogues without a per-tile
+// hook): each warp owns chunks of 32 consecutive rows dealt round-robin over
+// every warp of the grid.  The chunk's nonzeros are one contiguous range of
+// col_idx / values, so the warp stages it into its own shared-memory slice
+// with coalesced loads (all independent, issued back to back), then lane l
+// reduces row l from shared memory in the reference's add.reduceat order,
+// gathering x through the read-only path.  A chunk with more than kCsrCap
+// nonzeros (long rows) is reduced straight from global memory.  No CTA-wide
+// barrier, no producer warp: ~48 warps per SM stream independently (the
+// TMA-ring kernel ran at one CTA of 9 warps per SM in fp64).
+constexpr int kCsrThreads = 256;
+constexpr int kCsrWarps = kCsrThreads / 32;
+constexpr int kCsrCap = 384;   // staged nonzeros per warp chunk (avg <= 12 per row)
+
+template <typename E, typename = void> struct needs_tiles { static constexpr bool value = false; };
+template <typename E> struct needs_tiles<E, decltype((void)E::kNeedsTiles)> {
+  static constexpr bool value = E::kNeedsTiles;
+};
+
+template <typename T, typename E>
+__global__ void __launch_bounds__(kCsrThreads) k_csr_warp(CsrView<T> A, const T* __restrict__ x, E epi) {
+  extern __shared__ __align__(16) unsigned char csr_smem[];   // [warps][cap] T, then [warps][cap] int32
+  __shared__ EpiShared<T> es;
+  pdl_wait();
+  pdl_trigger();
+  if (epi.skip()) return;
+  epi.init(es, nullptr);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long n = A.n;
+  const long long nchunks = (n + 31) / 32;
+  const long long gw = (long long)blockIdx.x * kCsrWarps + warp;
+  const long long nw = (long long)gridDim.x * kCsrWarps;
+  T* v_s = reinterpret_cast<T*>(csr_smem) + (size_t)warp * kCsrCap;
+  int32_t* ci_s = reinterpret_cast<int32_t*>(csr_smem + sizeof(T) * kCsrWarps * kCsrCap) + (size_t)warp * kCsrCap;
+  for (long long c = gw; c < nchunks; c += nw) {
+    const long long r = c * 32 + lane;
+    const bool in = r < n;
+    const int lo = in ? __ldg(A.rp + r) : 0;
+    const int hi = in ? __ldg(A.rp + r + 1) : 0;
+    const long long rlast = min(c * 32 + 31, n - 1);
+    const int s = __shfl_sync(0xffffffffu, lo, 0);
+    const int e = __ldg(A.rp + rlast + 1);
+    const int cnt = e - s;
+    T y = T(0);
+    if (cnt <= kCsrCap) {
+      __syncwarp();   // the previous chunk's readers are done with the slice
+#pragma unroll 4
+      for (int i = lane; i < cnt; i += 32) {
+        ci_s[i] = __ldcs(A.ci + s + i);
+        v_s[i] = __ldcs(A.v + s + i);
+      }
+      __syncwarp();
+      if (in) {
+        const int32_t* cs = ci_s + (lo - s);
+        const T* vs = v_s + (lo - s);
+        auto get = [&](int i) -> T { return mul_rn(vs[i], __ldg(x + cs[i])); };
+        y = row_reduce<T>(get, hi - lo);
+      }
+    } else if (in) {
+      const int32_t* cg = A.ci + lo;
+      const T* vg = A.v + lo;
+      auto get = [&](int i) -> T { return mul_rn(__ldg(vg + i), __ldg(x + __ldg(cg + i))); };
+      y = row_reduce<T>(get, hi - lo);
+    }
+    if (in) epi.on_row(r, y);
+  }
+  epi.on_end();
+}
+
 // DIA packing + pattern check: one thread per row.  *bad != 0 when the CSR
 // pattern is not exactly the Dirichlet 5/7-point stencil of the grid.
 template <typename T>
@@ -473,6 +557,25 @@ __global__ void __launch_bounds__(kThreads) k_stencil_pack(int dims, int nx, lon
 template <typename T, typename E>
 static cudaError_t launch_matrix(const CsrView<T>& A, const T* x, const E& epi, size_t extra,
                                  cudaStream_t st) {
+  if constexpr (!needs_tiles<E>::value) {
+    if (csr_warp_enabled()) {
+      static std::once_flag once_w;
+      static int occ_w = 1;
+      constexpr size_t dsm = (size_t)kCsrWarps * kCsrCap * (sizeof(T) + 4);
+      std::call_once(once_w, [&] {
+        cudaFuncSetAttribute(k_csr_warp<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_csr_warp<T, E>, kCsrThreads, dsm);
+        cudaGetLastError();
+        if (occ_w < 1) occ_w = 1;
+      });
+      long long G = (A.n + 32LL * kCsrWarps - 1) / (32LL * kCsrWarps);
+      const long long cap = std::min<long long>((long long)num_sms() * occ_w, kMaxParts);
+      if (G > cap) G = cap;
+      if (G < 1) G = 1;
+      count_launch();
+      return launch_k(E::kPdl, false, k_csr_warp<T, E>, dim3((unsigned)G), dim3(kCsrThreads), dsm, st, A, x, epi);
+    }
+  }
   const size_t smem = sizeof(SpSmem<T>) + extra;
   static std::once_flag once;
   static int occ = 1;

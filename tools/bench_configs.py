@@ -110,9 +110,27 @@ def cfg5(reps):
                       round(min(f64["solve_s"]) / min(ir["solve_s"]), 3)}), flush=True)
 
 
+def spmv(reps):
+    """bench.spmv_bench (the reference's SpMV protocol, bench.py:82-119) on the config matrices."""
+    from paper_2109_01232_b200 import bench as B
+    for name, spec in (("laplace3d:150", P.StencilSpec(P.StencilKind.LAPLACE3D, 150)),
+                       ("convdiff2d:1500:c1501", P.StencilSpec(P.StencilKind.CONVDIFF2D, 1500, convection=1501.0)),
+                       ("laplace3d:200", P.StencilSpec(P.StencilKind.LAPLACE3D, 200))):
+        A = P.generate(spec)
+        r = B.spmv_bench(A, reps=200, trials=3, name=name)
+        print(json.dumps({"spmv_bench": name, "n": r.n, "nnz": r.nnz, "max_nnz_row": r.max_nnz_row,
+                          "t_fp64_per_product_us": round(r.t_fp64 / 200 * 1e6, 2),
+                          "t_fp32_per_product_us": round(r.t_fp32 / 200 * 1e6, 2),
+                          "measured_speedup": round(r.measured_speedup, 3), "predicted": round(r.predicted, 3),
+                          "quadrant": r.quadrant.value, "GBps_fp64": round(r.gbps_fp64, 1),
+                          "GBps_fp32": round(r.gbps_fp32, 1)}), flush=True)
+        del A
+        torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["cfg3", "cfg4", "cfg5", "all"])
+    ap.add_argument("which", choices=["cfg3", "cfg4", "cfg5", "spmv", "all"])
     ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
     for c in (("cfg3", "cfg4", "cfg5") if a.which == "all" else (a.which,)):
