@@ -319,7 +319,9 @@ def dist_arm(args, rank: int, world: int):
     # of this path with several ranks sharing one GPU (MPG_BENCH_BACKEND=gloo)
     coll = HostStagedCollectives() if _backend() == "gloo" else Collectives()
     crit = StopCriteria(rtol=RTOL, m=M)
-    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll)
+    # NVLink peer-memory halos written by the SCALE phase (MPG_PEER_HALO=0: NCCL send/recv)
+    peer = os.environ.get("MPG_PEER_HALO", "1") != "0"
+    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer)
 
     def solve():
         solver.x_buf.zero_()
@@ -348,7 +350,7 @@ def dist_arm(args, rank: int, world: int):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     from paper_2109_01232_b200.dist import dist_gmres_ir
-    rep_h = dist_gmres_ir(spec, part, coll, crit, b_local=b_host)
+    rep_h = dist_gmres_ir(spec, part, coll, crit, b_local=b_host, peer_halo=peer)
     x_host = rep_h.x.cpu().numpy()
     torch.cuda.synchronize()
     e2e = torch.tensor([time.perf_counter() - t0], device="cuda")
@@ -364,7 +366,9 @@ def dist_arm(args, rank: int, world: int):
         "config": {"workload": "gmres_ir laplace3d:150 GMRES(50) rtol=1e-10 (BASELINE configs[1]), "
                                "row-partitioned by z-planes",
                    "n": NX ** 3, "m": M, "rtol": RTOL, "parallelism": f"rows{world}",
-                   "collectives": "NCCL halo send/recv + 3 allreduces per Arnoldi step",
+                   "collectives": ("peer-memory halo stores fused into the basis scaling + " if solver.peer
+                                   else "NCCL halo send/recv + ") + "3 NCCL allreduces per Arnoldi step; "
+                                  "whole cycles replayed as CUDA graphs",
                    "l2": "working set >> L2 per rank at N<=8; no flush needed"},
         "iters": rep.total_iters, "iters_reference": REFERENCE_IR_ITERS,
         "storage": "stencil", "gpu_launches": launches, "clocks": clk.summary(),

@@ -48,6 +48,7 @@ extern "C" {
 #define MPG_FLAG_SINGULAR 4        /* krylov.py:198-201 SingularHessenberg   */
 #define MPG_FLAG_OVERFLOW 8        /* core.py:264-271   PrecisionOverflow    */
 #define MPG_FLAG_NONFINITE_X 16    /* solvers.py:350-352 DivergenceError     */
+#define MPG_FLAG_HALO_TIMEOUT 32   /* distributed peer halo: a neighbour's flag never arrived */
 
 /* stencil kinds (gen.py:34-41) */
 #define MPG_LAPLACE2D 0
@@ -294,6 +295,23 @@ typedef struct {
                              preconditioner buffers): the distributed halo, or zero padding
                              on one GPU; >= one grid plane enables the branchless stencil rows */
   int64_t dia_ld;         /* slot stride of dia/dia64/pc_dia (0: same as ldv) */
+  /* peer-memory halo (distributed mode, optional; all null = the caller
+   * exchanges halos).  The SCALE phase of step j writes the first / last
+   * `halo` rows of V[:, j+1] straight into the neighbours' halo rows (peer
+   * mappings over NVLink: cudaIpcOpenMemHandle / P2P) and then releases a
+   * sequence number into the neighbour's halo_flags; the SPMV phase of step
+   * j+1 waits on this rank's own flags.  The basis row j of a neighbour
+   * starts at peer_*_V + j * peer_*_ld; our rows land at offset peer_*_off
+   * from its owned block (prev: its n_local, upper halo; next: -halo). */
+  void* peer_prev_V;
+  int64_t peer_prev_ld;
+  int64_t peer_prev_off;
+  void* peer_next_V;
+  int64_t peer_next_ld;
+  int64_t peer_next_off;
+  uint32_t* halo_flags;     /* this rank's 2 flags: [0] written by prev, [1] by next */
+  uint32_t* peer_prev_flag; /* the prev rank's halo_flags + 1 */
+  uint32_t* peer_next_flag; /* the next rank's halo_flags + 0 */
 } mpg_solver_desc;
 
 /* Phases of one distributed restart cycle.  A phase marked

@@ -20,6 +20,7 @@ FP32, FP64 = 0, 1
 MODE_RESTARTED, MODE_IR = 0, 1
 PC_NONE, PC_JACOBI, PC_POLY = 0, 1, 2
 FLAG_NONFINITE_OP, FLAG_NONFINITE_GAMMA, FLAG_SINGULAR, FLAG_OVERFLOW, FLAG_NONFINITE_X = 1, 2, 4, 8, 16
+FLAG_HALO_TIMEOUT = 32
 POLY_SCALE, POLY_HORNER, POLY_ACC, POLY_NEWTON_REAL, POLY_PAIR1, POLY_PAIR2, POLY_ZERO = range(7)
 STENCIL_KIND = {"laplace2d": 0, "laplace3d": 1, "convdiff2d": 2, "stretched2d": 3,
                 "biharmonic2d": 4, "star2d": 5, "recirc2d": 6}
@@ -64,7 +65,10 @@ class SolverDesc(C.Structure):
                 ("stencil_dims", C.c_int32), ("stencil_nx", C.c_int32),
                 ("dia", C.c_void_p), ("dia64", C.c_void_p), ("pc_dia", C.c_void_p),
                 ("dist", C.c_int32), ("reserved_i", C.c_int32), ("row0", C.c_int64),
-                ("halo", C.c_int64), ("dia_ld", C.c_int64)]
+                ("halo", C.c_int64), ("dia_ld", C.c_int64),
+                ("peer_prev_V", C.c_void_p), ("peer_prev_ld", C.c_int64), ("peer_prev_off", C.c_int64),
+                ("peer_next_V", C.c_void_p), ("peer_next_ld", C.c_int64), ("peer_next_off", C.c_int64),
+                ("halo_flags", C.c_void_p), ("peer_prev_flag", C.c_void_p), ("peer_next_flag", C.c_void_p)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double

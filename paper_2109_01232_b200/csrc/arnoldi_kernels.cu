@@ -900,6 +900,97 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
   }
 }
 
+// ======================================= distributed: peer-memory halo (dist)
+// V[:, j+1] = w / h_sub (krylov.py:148) for this rank's rows, and the rows a
+// neighbour needs for its next SpMV written straight into its halo through
+// the peer mapping: our first `halo` rows go to prev's upper halo, our last
+// `halo` rows to next's lower halo.  After every CTA's stores are fenced
+// system-wide, the last CTA bumps this rank's halo sequence number (header
+// reserved1) and release-stores it into both neighbours' flags.
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_step_scale_peer(const T* __restrict__ w, T* __restrict__ vn,
+                                                              long long n, long long halo, int j,
+                                                              StateView<T> sv, T* prev_row, T* next_row,
+                                                              uint32_t* prev_flag, uint32_t* next_flag,
+                                                              unsigned int* counter) {
+  if (gated(sv.h)) return;
+  const T hs = sv.Hc(j, j + 1);
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+    const T v = div_rn(w[r], hs);
+    vn[r] = v;
+    if (prev_row && r < halo) prev_row[r] = v;
+    if (next_row && r >= n - halo) next_row[r - (n - halo)] = v;
+  }
+  __threadfence_system();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    *counter = 0u;
+    __threadfence_system();
+    volatile int32_t* seqp = &sv.h->reserved1;
+    const uint32_t seq = (uint32_t)(*seqp) + 1u;
+    *seqp = (int32_t)seq;
+    if (prev_flag) st_release_sys_u32(prev_flag, seq);
+    if (next_flag) st_release_sys_u32(next_flag, seq);
+  }
+}
+
+// Before the SpMV of step j >= 1: wait until both neighbours have released the
+// halo rows of V[:, j] (their sequence number caught up with ours).
+// Bounded: after ~20 s without the flag the cycle is stopped with
+// MPG_FLAG_HALO_TIMEOUT (raised on the host) instead of hanging the GPU.
+__global__ void k_halo_wait(mpg_state_header* h, const uint32_t* flags, int has_prev, int has_next) {
+  if (gated(h) || threadIdx.x != 0) return;
+  const uint32_t seq = (uint32_t)(*(volatile const int32_t*)&h->reserved1);
+  const unsigned long long t0 = clock64(), limit = 40ull * 1000 * 1000 * 1000;   // ~20 s at 2 GHz
+  for (int side = 0; side < 2; ++side) {
+    if (side == 0 ? !has_prev : !has_next) continue;
+    while ((int32_t)(ld_acquire_sys_u32(flags + side) - seq) < 0) {
+      if (clock64() - t0 > limit) {
+        h->flags |= MPG_FLAG_HALO_TIMEOUT;
+        h->done = 1;
+        __threadfence_system();
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+  __threadfence_system();
+}
+
+template <typename T>
+cudaError_t launch_step_scale_peer(const T* w, T* vn, long long n, long long halo, int j, StateView<T> sv,
+                                   T* prev_row, T* next_row, uint32_t* prev_flag, uint32_t* next_flag,
+                                   WsView ws, cudaStream_t st) {
+  count_launch();
+  long long G = (n + kThreads - 1) / kThreads;
+  const long long cap = (long long)num_sms() * 8;
+  if (G > cap) G = cap;
+  if (G < 1) G = 1;
+  k_step_scale_peer<T><<<(unsigned)G, kThreads, 0, st>>>(w, vn, n, halo, j, sv, prev_row, next_row, prev_flag,
+                                                         next_flag, ws.counter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_halo_wait(mpg_state_header* h, const uint32_t* flags, int has_prev, int has_next,
+                             cudaStream_t st) {
+  count_launch();
+  k_halo_wait<<<1, 32, 0, st>>>(h, flags, has_prev, has_next);
+  return cudaGetLastError();
+}
+
 // ===================================================================== start
 
 // Reset the cycle state (krylov.py:62-68, 96-100) — whole CTA.
@@ -1697,6 +1788,9 @@ cudaError_t launch_combine(const T* V, long long ldv, long long n, StateView<T> 
                                             cudaStream_t);                                     \
   template cudaError_t launch_update_norm_scale<T>(const T*, long long, long long, int, T*,     \
                                                    StateView<T>, WsView, int, cudaStream_t);   \
+  template cudaError_t launch_step_scale_peer<T>(const T*, T*, long long, long long, int,       \
+                                                 StateView<T>, T*, T*, uint32_t*, uint32_t*,   \
+                                                 WsView, cudaStream_t);                        \
   template cudaError_t launch_start<T>(const T*, long long, StateView<T>, double, const double*, \
                                        double, WsView, cudaStream_t);                          \
   template cudaError_t launch_start_scale<T>(const T*, T*, long long, StateView<T>,             \

@@ -345,6 +345,8 @@ static cudaError_t enqueue_phase(const mpg_solver& s, int phase, int j, int m_li
     case MPG_PH_START_SCALE:
       return launch_start_scale<T>(static_cast<const T*>(ir ? d.r_in : d.r), V, d.n, sv, st);
     case MPG_PH_SPMV_DOT:
+      if (j >= 1 && d.halo_flags && (d.peer_prev_V || d.peer_next_V))
+        TRY(launch_halo_wait(h, d.halo_flags, d.peer_prev_V ? 1 : 0, d.peer_next_V ? 1 : 0, st));
       if (split_spmv_dot1()) {
         TRY(with_matrix<T>(d, static_cast<const T*>(d.values), d.dia, [&](const auto& A) {
           return launch_spmv<T>(A, V + (size_t)j * d.ldv, w, ws, st);
@@ -365,6 +367,15 @@ static cudaError_t enqueue_phase(const mpg_solver& s, int phase, int j, int m_li
     case MPG_PH_POST_NORM:
       return launch_dist_post<T>(DP_POST_NORM, sv, j, m_limit, d.rtol, d.breakdown_tol, 0, st);
     case MPG_PH_SCALE:
+      if (d.halo_flags && (d.peer_prev_V || d.peer_next_V)) {
+        T* prow = d.peer_prev_V ? static_cast<T*>(d.peer_prev_V) + (size_t)(j + 1) * d.peer_prev_ld + d.peer_prev_off
+                                : nullptr;
+        T* nrow = d.peer_next_V ? static_cast<T*>(d.peer_next_V) + (size_t)(j + 1) * d.peer_next_ld + d.peer_next_off
+                                : nullptr;
+        return launch_step_scale_peer<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, d.halo, j, sv, prow, nrow,
+                                         d.peer_prev_V ? d.peer_prev_flag : nullptr,
+                                         d.peer_next_V ? d.peer_next_flag : nullptr, ws, st);
+      }
       return launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st);
     case MPG_PH_FINISH:
       return finish_cycle<T>(s, sv, ws, st);

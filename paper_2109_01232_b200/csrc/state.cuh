@@ -153,6 +153,14 @@ cudaError_t launch_start_scale(const T* r0, T* v0, long long n, StateView<T> sv,
 template <typename T>
 cudaError_t launch_lsq(StateView<T> sv, cudaStream_t st);
 
+// distributed peer-memory halo: scale + remote halo stores + flag release; flag wait
+template <typename T>
+cudaError_t launch_step_scale_peer(const T* w, T* vn, long long n, long long halo, int j, StateView<T> sv,
+                                   T* prev_row, T* next_row, uint32_t* prev_flag, uint32_t* next_flag,
+                                   WsView ws, cudaStream_t st);
+cudaError_t launch_halo_wait(mpg_state_header* h, const uint32_t* flags, int has_prev, int has_next,
+                             cudaStream_t st);
+
 // persistent per-step kernel (step_kernel.cu), stencil storage, single GPU
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& S, const T* x, T* V, long long ldv, long long n, int j,

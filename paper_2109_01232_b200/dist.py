@@ -179,7 +179,8 @@ class DistributedStencilSolver:
     for the rank's rows, packed with mpg_stencil_pack_rows)."""
 
     def __init__(self, spec, part: RowPartition, mode: str, m: int, rtol: float,
-                 collectives, precision: Precision = FP64, b_local=None, use_graph: bool = True):
+                 collectives, precision: Precision = FP64, b_local=None, use_graph: bool = True,
+                 peer_halo: bool = False, group=None):
         from .gen import generate_rows
         if mode not in ("ir", "restarted"):
             raise ValueError("mode must be 'ir' or 'restarted'")
@@ -247,9 +248,50 @@ class DistributedStencilSolver:
         d.dia = ptr(self._dia[self.prec])
         d.dia64 = ptr(self._dia[FP64]) if self.mode == _lib.MODE_IR else None
         d.dist, d.row0, d.halo = 1, part.row0, part.halo
+        self.peer = bool(peer_halo) and part.world > 1
+        if self.peer:
+            try:
+                self._setup_peer_halo(d, group)
+            except Exception as exc:  # pragma: no cover - depends on the node's IPC/P2P support
+                import warnings
+                warnings.warn(f"peer-memory halo unavailable ({exc}); using collective halo exchange",
+                              stacklevel=2)
+                self.peer = False
+                d.peer_prev_V = d.peer_next_V = d.halo_flags = None
+                d.peer_prev_flag = d.peer_next_flag = None
         h = C.c_void_p()
         _lib.call("mpg_solver_create", C.byref(d), C.byref(h))
         self.handle, self.desc = h, d
+
+    def _setup_peer_halo(self, d, group) -> None:
+        """Map the neighbours' basis buffers and halo flags into this process
+        (CUDA IPC handles exchanged over the process group; on one node the
+        mappings are NVLink peer memory) so the SCALE phase can store the
+        boundary planes of each new basis vector straight into their halos."""
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+        part, s = self.part, self.prec.dtype.itemsize
+        self.halo_flags = torch.zeros(2, dtype=torch.int32, device=self.V_buf.device)
+        info = {"V": reduce_tensor(self.V_buf)[1], "flags": reduce_tensor(self.halo_flags)[1],
+                "ld": part.ld, "n": part.n_local, "o": part.own_offset}
+        infos = [None] * part.world
+        dist.all_gather_object(infos, info, group=group)
+        self._peer_maps = []
+
+        def open_peer(r):
+            v = rebuild_cuda_tensor(*infos[r]["V"])
+            f = rebuild_cuda_tensor(*infos[r]["flags"])
+            self._peer_maps += [v, f]
+            return v.data_ptr() + infos[r]["o"] * s, f.data_ptr(), infos[r]
+        d.halo_flags = ptr(self.halo_flags)
+        if part.prev is not None:
+            vp, fp, inf = open_peer(part.prev)
+            d.peer_prev_V, d.peer_prev_ld, d.peer_prev_off = vp, inf["ld"], inf["n"]   # its upper halo
+            d.peer_prev_flag = fp + 4                                                   # its flags[1]
+        if part.next is not None:
+            vp, fp, inf = open_peer(part.next)
+            d.peer_next_V, d.peer_next_ld, d.peer_next_off = vp, inf["ld"], -part.halo  # its lower halo
+            d.peer_next_flag = fp                                                       # its flags[0]
 
     # --- helpers
     def close(self):
@@ -330,7 +372,8 @@ class DistributedStencilSolver:
         self._ph("POST_START", 0, m_limit)
         self._ph("START_SCALE", 0, m_limit)
         for j in range(m_limit):
-            self.coll.halo_(self.V_row(j), self.part)
+            if j == 0 or not self.peer:      # with peer halos SCALE has already written them
+                self.coll.halo_(self.V_row(j), self.part)
             self._ph("SPMV_DOT", j, m_limit)
             self.coll.allreduce_(self.red[: j + 3])
             self._ph("POST_DOT1", j, m_limit)
@@ -390,12 +433,12 @@ def _dist_solve(solver: DistributedStencilSolver, criteria: StopCriteria, ir: bo
 
 
 def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
-                  b_local=None, *, timer=None, use_graph: bool = True) -> SolveReport:
+                  b_local=None, *, timer=None, use_graph: bool = True, peer_halo: bool = False) -> SolveReport:
     """Row-partitioned GMRES-IR (solvers.py:297-384); x returned as this
     rank's owned block (device tensor)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "ir", criteria.m, criteria.rtol, collectives,
-                                 b_local=b_local, use_graph=use_graph)
+                                 b_local=b_local, use_graph=use_graph, peer_halo=peer_halo)
     try:
         return _dist_solve(s, criteria, True, timer)
     finally:
@@ -404,11 +447,12 @@ def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria 
 
 def dist_gmres_restarted(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
                          precision: Precision = FP64, b_local=None, *, timer=None,
-                         use_graph: bool = True) -> SolveReport:
+                         use_graph: bool = True, peer_halo: bool = False) -> SolveReport:
     """Row-partitioned GMRES(m) in one precision (solvers.py:251-294)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "restarted", criteria.m, criteria.rtol, collectives,
-                                 precision=precision, b_local=b_local, use_graph=use_graph)
+                                 precision=precision, b_local=b_local, use_graph=use_graph,
+                                 peer_halo=peer_halo)
     try:
         return _dist_solve(s, criteria, False, timer)
     finally:

@@ -42,7 +42,7 @@ LOSS_OF_ACCURACY_FACTOR = 10.0   # solvers.py:51
 STALL_IMPROVEMENT = 0.01         # solvers.py:55
 STALL_RESTARTS = 2               # solvers.py:56
 _ERROR_FLAGS = (_lib.FLAG_NONFINITE_OP | _lib.FLAG_NONFINITE_GAMMA | _lib.FLAG_SINGULAR |
-                _lib.FLAG_OVERFLOW | _lib.FLAG_NONFINITE_X)
+                _lib.FLAG_OVERFLOW | _lib.FLAG_NONFINITE_X | _lib.FLAG_HALO_TIMEOUT)
 
 
 @dataclass(frozen=True)
@@ -326,6 +326,8 @@ def _raise_flags(hdr, total: int, ir: bool) -> None:
     f = hdr.flags
     if not f & _ERROR_FLAGS:
         return
+    if f & _lib.FLAG_HALO_TIMEOUT:
+        raise RuntimeError("distributed peer halo: a neighbour's halo flag did not arrive within 20 s")
     if f & _lib.FLAG_OVERFLOW:
         raise PrecisionOverflowError("an entry of the scaled residual overflows fp32")
     if f & (_lib.FLAG_NONFINITE_OP | _lib.FLAG_NONFINITE_GAMMA):

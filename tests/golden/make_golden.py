@@ -5,6 +5,7 @@ Run in the build container, where the read-only reference exists:
     python tests/golden/make_golden.py            # small + assembly hashes
     python tests/golden/make_golden.py --cfg2     # + full Laplace3D(150) runs (~35 min)
     python tests/golden/make_golden.py --skip-small --cfg3   # ConvDiff2D(1500) runs (~28 min)
+    python tests/golden/make_golden.py --skip-small --cfg4 25  # Laplace3D(200) IR+poly(25) (~1 h)
 
 Nothing on the GPU box reads /root/reference: the tests only read the
 committed JSON/NPZ written here.  The reference is imported read-only from
@@ -96,6 +97,11 @@ CFG3_RUNS = [  # BASELINE configs[2]: UniFlow2D 1500^2 (convection
 ]
 
 
+CFG4_RUNS = {  # BASELINE configs[3]: GMRES-IR + GMRES-polynomial(d) on Laplace3D 200^3
+    d: (f"laplace3d:200/ir+poly{d}/m50", ("laplace3d", 200, {}), f"ir+poly{d}", {"m": 50}) for d in (25, 40)
+}
+
+
 def run_one(mp, spec, solver, kw):
     kind, nx, sk = spec
     A = mp.generate(mp.StencilSpec(mp.StencilKind(kind), nx, **sk))
@@ -166,6 +172,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--cfg3", action="store_true")
+    ap.add_argument("--cfg4", type=int, choices=[25, 40], default=None)
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
     mp = _ref()
@@ -205,6 +212,13 @@ def main():
             runs[name] = report_dict(run_one(mp, spec, solver, kw))
             print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg3.json"), "w") as f:
+            json.dump({"meta": meta, "runs": runs}, f, indent=1)
+    if args.cfg4:
+        name, spec, solver, kw = CFG4_RUNS[args.cfg4]
+        t = time.time()
+        runs = {name: report_dict(run_one(mp, spec, solver, kw))}
+        print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
+        with open(os.path.join(HERE, f"reference_cfg4_poly{args.cfg4}.json"), "w") as f:
             json.dump({"meta": meta, "runs": runs}, f, indent=1)
 
 

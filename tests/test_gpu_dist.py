@@ -153,3 +153,51 @@ def test_nccl_world1_graph_captured_cycle_bitwise_equals_fused(mode):
         assert iters == ref.total_iters and conv == ref.converged
         assert np.array_equal(x, ref.x.cpu().numpy())
         assert hist == [tuple(e) for e in ref.residual_history]
+
+
+def _rank_peer(rank, world, port, kind, nx, mode, peer, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = P.StencilSpec(P.StencilKind(kind), nx)
+        dims = 3 if kind == "laplace3d" else 2
+        part = RowPartition.for_stencil(dims, nx, world, rank)
+        crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=600)
+        coll = HostStagedCollectives()
+        f = dist_gmres_ir if mode == "ir" else dist_gmres_restarted
+        rep = f(spec, part, coll, crit, peer_halo=peer)
+        dist.barrier()
+        out.put((rank, rep.total_iters, [tuple(e) for e in rep.residual_history], rep.x.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,nx,mode", [(2, "laplace3d", 16, "ir"), (3, "laplace2d", 40, "fp64")])
+def test_peer_memory_halo_bitwise_equals_collective_halo(world, kind, nx, mode):
+    """The SCALE phase writes each new basis vector's boundary planes straight
+    into the neighbours' halos through CUDA IPC peer mappings and releases a
+    sequence flag; the SpMV of the next step waits on it.  Ranks share one GPU
+    here (on the multi-GPU box the same mappings are NVLink peer memory).  The
+    transport must not change a bit: same iterations, histories and x as the
+    collective halo exchange."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    res = {}
+    for peer in (False, True):
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_rank_peer, args=(r, world, port, kind, nx, mode, peer, q))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        got = sorted((q.get(timeout=600) for _ in procs), key=lambda t: t[0])
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        res[peer] = got
+    for a, b in zip(res[False], res[True]):
+        assert a[1] == b[1] and a[2] == b[2]
+        assert np.array_equal(a[3], b[3])
