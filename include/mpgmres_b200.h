@@ -289,7 +289,10 @@ typedef struct {
   /* row-partitioned (distributed) mode, driven phase by phase through
    * mpg_solver_phase with the caller's collectives in between */
   int32_t dist;           /* 1: this handle is one rank of a row partition */
-  int32_t reserved_i;
+  int32_t step_kernel;    /* 0 auto: one persistent cooperative kernel per Arnoldi step for
+                             small vectors (n * sizeof(T) <= 20 MB; stencil storage, no
+                             preconditioner, one GPU), else four launches; 1 four launches;
+                             2 persistent whenever it applies */
   int64_t row0;           /* global index of local row 0 */
   int64_t halo;           /* readable rows on each side of every SpMV input (V rows, x,
                              preconditioner buffers): the distributed halo, or zero padding

@@ -64,7 +64,7 @@ class SolverDesc(C.Structure):
                 ("pc_t3", C.c_void_p), ("pc_t4", C.c_void_p),
                 ("stencil_dims", C.c_int32), ("stencil_nx", C.c_int32),
                 ("dia", C.c_void_p), ("dia64", C.c_void_p), ("pc_dia", C.c_void_p),
-                ("dist", C.c_int32), ("reserved_i", C.c_int32), ("row0", C.c_int64),
+                ("dist", C.c_int32), ("step_kernel", C.c_int32), ("row0", C.c_int64),
                 ("halo", C.c_int64), ("dia_ld", C.c_int64),
                 ("peer_prev_V", C.c_void_p), ("peer_prev_ld", C.c_int64), ("peer_prev_off", C.c_int64),
                 ("peer_next_V", C.c_void_p), ("peer_next_ld", C.c_int64), ("peer_next_off", C.c_int64),

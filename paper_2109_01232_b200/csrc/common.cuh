@@ -53,7 +53,11 @@ __device__ __forceinline__ void vload(const T* p, T (&v)[Vec<T>::n]) {
 // streaming (evict-first) load: for data read exactly once per kernel
 template <typename T>
 __device__ __forceinline__ void vload_cs(const T* p, T (&v)[Vec<T>::n]) {
+#ifdef MPG_BASIS_LDG
+  auto q = __ldg(reinterpret_cast<const typename Vec<T>::type*>(p));   // A/B: keep the basis in L2
+#else
   auto q = __ldcs(reinterpret_cast<const typename Vec<T>::type*>(p));
+#endif
   if constexpr (Vec<T>::n == 4) { v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w; }
   else { v[0] = q.x; v[1] = q.y; }
 }

@@ -239,12 +239,15 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   T* wbuf[2] = {w, fuse ? static_cast<T*>(d.u) : w};
   // single-GPU stencil storage without a preconditioner: one persistent
   // cooperative kernel per Arnoldi step (step_kernel.cu) when it applies
-  const bool mega = mega_enabled() && !fuse && d.pc_kind == MPG_PC_NONE && !d.dist && d.stencil_dims &&
-                    d.dia && d.halo >= (d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx
-                                                            : (long long)d.stencil_nx);
+  const bool mega_ok = !fuse && d.pc_kind == MPG_PC_NONE && !d.dist && d.stencil_dims && d.dia &&
+                       d.halo >= (d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx
+                                                      : (long long)d.stencil_nx);
+  int sk = d.step_kernel;
+  if (mega_env() >= 0) sk = mega_env() ? 2 : 1;
+  const bool mega = mega_ok && (sk == 2 || (sk == 0 && (double)d.n * sizeof(T) <= 20e6));
   for (int j = 0; j < m_limit; ++j) {
     T* wj = wbuf[j & 1];
-    if (mega && j + 3 <= 72) {
+    if (mega && j + 1 <= kMegaMaxK) {
       ProfScope ps(PK_STEP);
       StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
                        d.stencil_dims, d.row0};

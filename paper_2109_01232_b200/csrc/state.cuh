@@ -161,11 +161,13 @@ cudaError_t launch_step_scale_peer(const T* w, T* vn, long long n, long long hal
 cudaError_t launch_halo_wait(mpg_state_header* h, const uint32_t* flags, int has_prev, int has_next,
                              cudaStream_t st);
 
-// persistent per-step kernel (step_kernel.cu), stencil storage, single GPU
+// persistent per-step kernel (step_kernel.cu), stencil storage, single GPU;
+// steps with k > kMegaMaxK basis vectors use the four-launch step
+constexpr int kMegaMaxK = 56;
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& S, const T* x, T* V, long long ldv, long long n, int j,
                              T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st);
-bool mega_enabled();   // MPG_MEGA=0 selects the four-launch step
+int mega_env();   // MPG_MEGA: 1 / 0 forces the persistent / four-launch step, -1 unset
 
 // distributed-mode post phases (k_dist_post)
 enum DistPostPhase {

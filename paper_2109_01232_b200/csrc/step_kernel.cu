@@ -357,17 +357,21 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
 
 // ------------------------------------------------------------------ launch
 
-// Off by default (MPG_MEGA=1 enables): measured on B200 at cfg2 the persistent
-// step ties the four-launch step in fp32 (IR solve 0.501 s vs 0.503 s) and
-// loses in fp64 (1.123 s vs 0.999 s: 64-register cap at 1024 threads spills,
-// one CTA per SM); the three grid barriers cost what the launch boundaries did.
-bool mega_enabled() {
-  static int v = -1;
-  if (v < 0) {
+// MPG_MEGA=1 / 0 forces the persistent / four-launch step for every solver
+// (A/B runs); unset (-1) leaves the choice to the descriptor (step_kernel).
+// Measured on B200 (IR solves, Laplace3D): the persistent step wins while the
+// launch and reduction-tail costs are a large share of a step -- nx 60: 15.1 vs
+// 19.2 ms, nx 75: 32.3 vs 39.5 ms, nx 100: 89 vs 100 ms, nx 126: 241 vs 247 ms
+// (fp64 nx 126: 453 vs 472 ms) -- ties at cfg2 fp32 (0.501 vs 0.503 s) and loses
+// at cfg2 fp64 (1.123 vs 0.999 s: 64-register cap at 1024 threads spills, one
+// CTA per SM).  Hence the 20 MB vector-size rule in solver.cu.
+int mega_env() {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("MPG_MEGA");
-    v = (e && e[0] == '1') ? 1 : 0;
+    v = e ? (e[0] == '1' ? 1 : 0) : -1;
   }
-  return v == 1;
+  return v;
 }
 
 template <typename T, int S, int KV, bool CACHE>
@@ -412,7 +416,7 @@ template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n, int j,
                              T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
   const int k = j + 1;
-  if (k + 2 > kMegaMaxCols || !SV.padded || SV.xdiv) return cudaErrorInvalidValue;
+  if (k > kMegaMaxK || k + 2 > kMegaMaxCols || !SV.padded || SV.xdiv) return cudaErrorInvalidValue;
   const int kv = (k + 7) / 8;
 #define MEGA_CASE(KVV)                                                                            \
   case KVV:                                                                                       \

@@ -18,6 +18,8 @@ as a CUDA tensor).
 
 from __future__ import annotations
 
+import contextlib
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Callable, NamedTuple
@@ -203,6 +205,25 @@ def _prepare_precond(M, A: CsrMatrix, solve_prec: Precision) -> _Prepared | None
     raise TypeError(f"unsupported preconditioner type {type(M).__name__}")
 
 
+_STEP_KERNEL = {"auto": 0, "split": 1, "persistent": 2}
+_step_kernel_mode = "auto"
+
+
+@contextlib.contextmanager
+def step_kernel(mode: str):
+    """Select the Arnoldi-step implementation of solvers created inside the
+    block: "auto" (default: the persistent per-step kernel for small vectors),
+    "split" (four launches per step) or "persistent" (csrc/step_kernel.cu)."""
+    global _step_kernel_mode
+    if mode not in _STEP_KERNEL:
+        raise ValueError(f"step kernel must be one of {sorted(_STEP_KERNEL)}")
+    prev, _step_kernel_mode = _step_kernel_mode, mode
+    try:
+        yield
+    finally:
+        _step_kernel_mode = prev
+
+
 class NativeSolve:
     """Device buffers + a native solver handle for one restarted solve.
 
@@ -242,6 +263,7 @@ class NativeSolve:
                               device=device())
         d = _lib.SolverDesc()
         d.mode, d.prec, d.m, d.use_graph = mode, prec.code, m, 1 if use_graph else 0
+        d.step_kernel = _STEP_KERNEL[_step_kernel_mode]
         d.n, d.ldv, d.rtol = n, self.ldv, float(rtol)
         d.breakdown_tol = 10.0 * prec.unit_roundoff
         d.row_ptr, d.col_idx, d.values = ptr(A.row_ptr), ptr(A.col_idx), ptr(A.values)

@@ -33,12 +33,16 @@ def test_world1_phase_pipeline_bitwise_equals_fused(kind, nx, mode):
     crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=3000)
     A = P.generate(spec)
     b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    # the distributed phases are the four-launch step's kernels in dist mode
+    split = P.solvers.step_kernel("split")
     if mode == "ir":
-        ref = P.gmres_ir(A, b, criteria=crit)
+        with split:
+            ref = P.gmres_ir(A, b, criteria=crit)
         rep = dist_gmres_ir(spec, part, NullCollectives(), crit)
     else:
         prec = P.FP64 if mode == "fp64" else P.FP32
-        ref = P.gmres_restarted(A, b, criteria=crit, precision=prec)
+        with split:
+            ref = P.gmres_restarted(A, b, criteria=crit, precision=prec)
         rep = dist_gmres_restarted(spec, part, NullCollectives(), crit, precision=prec)
         if prec is P.FP32:
             rep.x = rep.x.to(torch.float64)
@@ -142,7 +146,8 @@ def test_nccl_world1_graph_captured_cycle_bitwise_equals_fused(mode):
     A = P.generate(P.StencilSpec(P.StencilKind(kind), nx))
     b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
     crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=3000)
-    ref = P.gmres_ir(A, b, criteria=crit) if mode == "ir" else P.gmres_restarted(A, b, criteria=crit)
+    with P.solvers.step_kernel("split"):
+        ref = P.gmres_ir(A, b, criteria=crit) if mode == "ir" else P.gmres_restarted(A, b, criteria=crit)
     for use_graph in (True, False):
         q = ctx.Queue()
         p = ctx.Process(target=_nccl_world1, args=(q, kind, nx, mode, use_graph))
