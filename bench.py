@@ -112,6 +112,9 @@ def cycle_bytes(n: int, nnz: int, m: int, s: int, storage: str = "csr") -> dict[
         "update_dot": sum((k + 2) * n * s for k in ks),       # read V[0..k) + w, write w
         "update_norm_givens": sum((k + 2) * n * s for k in ks),
         "scale": m * 2 * n * s,
+        # persistent per-step kernel: matrix + v_j once, V[0..k) three sweeps, v_{j+1}
+        # written; w never leaves shared memory
+        "step": sum(spmv + 3 * k * n * s for k in ks),
     }
 
 
@@ -204,10 +207,10 @@ def native_arm(args, rank: int, world: int):
         model = cycle_bytes(n, nnz, M, 4, used)
         if prof.get("dot1", (0.0, 0))[1] > 0:
             model = split_cycle_bytes(model, n, nnz, M, 4, used)
-        if prof.get("scale", (0.0, 0))[1] == 0:
-            # K_S fused into K_C (k_update_norm_scale): read V + w', write v = (k+2) n s,
-            # the same count as update_norm_givens; no separate scale traffic
-            model.pop("scale")
+        # only the classes this cycle actually launched
+        model = {k: v for k, v in model.items() if prof.get(k, (0.0, 0))[1] > 0}
+        # (K_S fused into K_C: "scale" has no launches and drops out above; the fused
+        # kernel's read V + w', write v = (k+2) n s is update_norm_givens' count)
         kernels = {}
         for k, (ms, cnt) in prof.items():
             kernels[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}

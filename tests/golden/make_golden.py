@@ -6,6 +6,7 @@ Run in the build container, where the read-only reference exists:
     python tests/golden/make_golden.py --cfg2     # + full Laplace3D(150) runs (~35 min)
     python tests/golden/make_golden.py --skip-small --cfg3   # ConvDiff2D(1500) runs (~28 min)
     python tests/golden/make_golden.py --skip-small --cfg4 25  # Laplace3D(200) IR+poly(25) (~1 h)
+    python tests/golden/make_golden.py --skip-small --cfg5     # Laplace3D(400): assembly + 1 IR cycle
 
 Nothing on the GPU box reads /root/reference: the tests only read the
 committed JSON/NPZ written here.  The reference is imported read-only from
@@ -173,6 +174,7 @@ def main():
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--cfg3", action="store_true")
     ap.add_argument("--cfg4", type=int, choices=[25, 40], default=None)
+    ap.add_argument("--cfg5", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
     mp = _ref()
@@ -213,6 +215,22 @@ def main():
             print(f"{name}: {runs[name]['total_iters']} it ({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg3.json"), "w") as f:
             json.dump({"meta": meta, "runs": runs}, f, indent=1)
+    if args.cfg5:
+        # BASELINE configs[4] (64M rows): a full reference solve is ~40 CPU-hours,
+        # so pin the assembly (sha256) and the first GMRES-IR cycle (50 fp32
+        # iterations + the fp64 residual) at full size
+        t = time.time()
+        A = mp.generate(mp.StencilSpec(mp.StencilKind("laplace3d"), 400))
+        asm = {"n": A.n_rows, "nnz": A.nnz, "row_ptr": sha(A.row_ptr), "col_idx": sha(A.col_idx),
+               "values": sha(A.values)}
+        print("cfg5 assembly", asm, f"({time.time() - t:.1f}s)", flush=True)
+        b = np.ones(A.n_rows)
+        rep = mp.gmres_ir(A, b, criteria=mp.StopCriteria(rtol=1e-10, m=50, max_iters=50))
+        runs = {"laplace3d:400/ir/m50/max50": report_dict(rep)}
+        print("cfg5 one IR cycle", runs["laplace3d:400/ir/m50/max50"]["boundaries"],
+              f"({time.time() - t:.1f}s)", flush=True)
+        with open(os.path.join(HERE, "reference_cfg5.json"), "w") as f:
+            json.dump({"meta": meta, "assembly": asm, "runs": runs}, f, indent=1)
     if args.cfg4:
         name, spec, solver, kw = CFG4_RUNS[args.cfg4]
         t = time.time()

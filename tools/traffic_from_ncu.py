@@ -18,14 +18,24 @@ import re
 import sys
 
 CLASSES = [  # (bench class, kernel-name pattern)
-    ("spmv_dot1", r"k_stencil<float, mpg::EpiPlain|k_spmv<float, mpg::EpiPlain"),
-    ("dot1", r"k_dot1_wo<float"),
-    ("update_dot", r"k_update_dot_w<float|k_update_dot<float"),
+    ("spmv_dot1", r"k_stencil<float, mpg::EpiPlain|k_spmv<float, mpg::EpiPlain|k_csr_warp<float, mpg::EpiPlain"),
+    ("dot1", r"k_dot1_wo<float|k_dot1_small<float"),
+    ("update_dot", r"k_update_dot_w<float|k_update_dot<float|k_update_dot_small<float"),
     ("update_norm_givens", r"k_update_norm_scale<float|k_update_norm<float"),
+    ("step", r"k_step_mega<float"),
 ]
 
 
-def main(path):
+def main(*paths):
+    """Several captures (e.g. the persistent-step and the four-launch cycle) merge by class."""
+    merged = {"sources": list(paths), "cache_control": "all (L2 flushed before each launch)", "classes": {}}
+    for p in paths:
+        merged["classes"].update(_classes(p))
+    json.dump(merged, sys.stdout, indent=1)
+    print()
+
+
+def _classes(path):
     rows = list(csv.reader(open(path)))
     hdr, recs = None, []
     for r in rows:
@@ -42,7 +52,7 @@ def main(path):
     # the last cycle: from the last k_start_ir (IR cycle start) to the end
     starts = [i for i, it in enumerate(items) if "k_start_ir" in it["name"]]
     cyc = items[starts[-1]:] if starts else items
-    out = {"source": path, "cache_control": "all (L2 flushed before each launch)", "classes": {}}
+    out = {"classes": {}}
     for cls, pat in CLASSES:
         sel = [it for it in cyc if re.search(pat, it["name"])]
         if not sel:
@@ -53,9 +63,8 @@ def main(path):
         out["classes"][cls] = {"launches": len(sel), "dram_bytes_per_launch": (rd + wr) / len(sel),
                                "dram_read_per_launch": rd / len(sel), "dram_write_per_launch": wr / len(sel),
                                "ncu_ns_per_launch": t / len(sel)}
-    json.dump(out, sys.stdout, indent=1)
-    print()
+    return out["classes"]
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(*sys.argv[1:])
