@@ -27,9 +27,15 @@ def main(path):
                 i = h.index(w)
                 print(f"  {w}: {r[i][:100]} {units[i]}")
         if "dram__bytes_read.sum" in h:
-            t = float(r[h.index("gpu__time_duration.sum")].replace(",", ""))
-            b = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) + float(r[h.index("dram__bytes_write.sum")].replace(",", ""))
-            print(f"  => DRAM GB/s (traffic/duration, units as listed): {b / t * 1e3:.1f}")
+            scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
+                     "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
+            def val(name):
+                i = h.index(name)
+                return float(r[i].replace(",", "")) * scale.get(units[i], 1.0)
+            t = val("gpu__time_duration.sum")
+            b = val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+            print(f"  => DRAM GB/s (traffic/duration): {b / t / 1e9:.1f}")
 
 
 if __name__ == "__main__":
