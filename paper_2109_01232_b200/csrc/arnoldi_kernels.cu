@@ -1,13 +1,17 @@
 // CGS2 Arnoldi kernels (krylov.py:112-202, solvers.py:122-174).
 //
-// One Arnoldi step j (k = j + 1 basis vectors) is four launches:
-//   K_A  spmv_dot1     w = A z, ||w||, finite check, c1 = V^T w      (spmv_kernels.cu)
-//   K_B  update_dot    w <- w - V c1 ; c2 = V^T w ; H[:,j] = c1 + c2   (this file, TMA-staged)
-//   K_C  update_norm   w <- w - V c2 ; h_sub = ||w|| ; breakdown ;
-//                      Givens rotation ; implicit residual ; done flag (this file)
-//   K_S  step_scale    V[:, j+1] = w / h_sub                          (this file)
+// The four-launch Arnoldi step j (k = j + 1 basis vectors):
+//   K_A1 SpMV          w = A z                                (spmv_kernels.cu)
+//   K_A2 dot1          ||w||, finite check, c1 = V^T w        (k_dot1_wo / k_dot1_small)
+//   K_B  update_dot    w <- w - V c1 ; c2 = V^T w ; H[:,j] = c1 + c2
+//                      (k_update_dot_w / k_update_dot_small; TMA-staged k_update_dot for k > 64)
+//   K_CS update_norm   w <- w - V c2 ; h_sub = ||w|| ; breakdown ; Givens rotation ;
+//        + scale       implicit residual ; done flag ; V[:, j+1] = w / h_sub
+//                      (cooperative k_update_norm_scale; k_update_norm + k_step_scale in
+//                      distributed mode, where an allreduce sits between them)
 // so the basis is swept three times per step (the reference's BLAS sequence
-// sweeps it four times).
+// sweeps it four times).  step_kernel.cu fuses the whole step into one
+// persistent launch for small vectors.
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -130,187 +134,6 @@ __global__ void __launch_bounds__(kUdThreads) k_update_dot(const T* __restrict__
         sv.c2[c] = s2;
         // h = 0; h += c1; h += c2  (krylov.py:137-141)
         sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);
-      }
-    }
-  }
-}
-
-// ===================================== K_B, register variant (k <= KT <= 64)
-// Thread-per-row: the k basis values of a row are loaded once into
-// registers, used for w' = w - V c1 and then for the c2 accumulators
-// (KT per thread), so V streams from HBM exactly once with coalesced loads
-// and no shared-memory staging.  One CTA-level reduction at the end.
-template <typename T, int KT>
-__global__ void __launch_bounds__(kThreads) k_update_dot_reg(const T* __restrict__ V, long long ldv,
-                                                             long long n, int k, T* __restrict__ w,
-                                                             StateView<T> sv, WsView ws) {
-  if (gated(sv.h)) return;
-  constexpr int ROWS = KT <= 4 ? 4 : (KT <= 8 ? 2 : 1);
-  __shared__ T c1s[KT];
-  __shared__ T red2[kWarps][KT];
-  __shared__ bool lastflag;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < KT) c1s[tid] = tid < k ? sv.c1[tid] : T(0);
-  __syncthreads();
-  long long R0, R1;
-  cta_rows(n, R0, R1);
-  T acc[KT];
-#pragma unroll
-  for (int i = 0; i < KT; ++i) acc[i] = T(0);
-  for (long long rb = R0 + tid; rb < R1; rb += (long long)kThreads * ROWS) {
-    T v[ROWS][KT];
-    T wv[ROWS];
-#pragma unroll
-    for (int q = 0; q < ROWS; ++q) {
-      const long long r = rb + (long long)q * kThreads;
-      const bool ok = r < R1;
-      wv[q] = ok ? w[r] : T(0);
-#pragma unroll
-      for (int i = 0; i < KT; ++i) v[q][i] = (ok && i < k) ? __ldcs(V + (size_t)i * ldv + r) : T(0);
-    }
-#pragma unroll
-    for (int q = 0; q < ROWS; ++q) {
-      const long long r = rb + (long long)q * kThreads;
-      T u = T(0);
-#pragma unroll
-      for (int i = 0; i < KT; ++i)
-        if (i < k) u = fma_rn(v[q][i], c1s[i], u);
-      const T x = sub_rn(wv[q], u);
-      if (r < R1) w[r] = x;
-#pragma unroll
-      for (int i = 0; i < KT; ++i)
-        if (i < k) acc[i] = fma_rn(v[q][i], x, acc[i]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < KT; ++i) {
-    if (i < k) {
-      const T a = warp_sum(acc[i]);
-      if (lane == 0) red2[warp][i] = a;
-    }
-  }
-  __syncthreads();
-  T* part = static_cast<T*>(ws.part);
-  if (tid < k) {
-    T s = T(0);
-    for (int q = 0; q < kWarps; ++q) s += red2[q][tid];
-    part[(size_t)blockIdx.x * k + tid] = s;
-  }
-  if (last_cta(ws.counter)) {
-    const int j = k - 1;
-    for (int c = warp; c < k; c += kWarps) {
-      T s2 = T(0);
-      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
-        sv.c2[c] = s2;
-        sv.Hc(j, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
-      }
-    }
-  }
-  (void)lastflag;
-}
-
-// ========================= K_B, quad-split register variant (k <= KT <= 64)
-// The 4 lanes of a quad share a 2-row segment; lane j owns basis vectors
-// i = 4q + j.  Each lane loads its vectors' 2-row slices once (8/16-byte
-// loads; the quad together reads a contiguous 2-row segment of 4 vectors),
-// forms its part of u = V c1, the quad completes u with two xor-shuffles,
-// every lane applies w' = w - u and accumulates its KT/4 pass-2 dots.  KT/4
-// accumulators per thread (instead of KT) keep occupancy high, so enough
-// loads are in flight to stream V at HBM rate.
-template <typename T, int KT>
-__global__ void __launch_bounds__(kThreads) k_update_dot_q(const T* __restrict__ V, long long ldv,
-                                                           long long n, int k, T* __restrict__ w,
-                                                           StateView<T> sv, WsView ws) {
-  if (gated(sv.h)) return;
-  constexpr int KQ = KT / 4;
-  __shared__ T c1s[KT];
-  __shared__ T red2[kWarps][KT];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int j = tid & 3, quad = tid >> 2;
-  if (tid < KT) c1s[tid] = tid < k ? sv.c1[tid] : T(0);
-  __syncthreads();
-  T c1q[KQ], acc[KQ];
-#pragma unroll
-  for (int q = 0; q < KQ; ++q) {
-    c1q[q] = c1s[4 * q + j];
-    acc[q] = T(0);
-  }
-  long long R0, R1;
-  cta_rows(n, R0, R1);
-  // warp-uniform trip count (the quad shuffles below need every lane)
-  for (long long wb = R0 + 16 * warp; wb < R1; wb += 2 * (kThreads / 4)) {
-    const long long rb = wb + 2 * (quad & 7);
-    const bool one = rb < R1;
-    const bool two = rb + 1 < R1;
-    T v0[KQ], v1[KQ];
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      const int i = 4 * q + j;
-      v0[q] = T(0);
-      v1[q] = T(0);
-      if (i < k && one) {
-        const T* p = V + (size_t)i * ldv + rb;
-        if (two) {
-          if constexpr (sizeof(T) == 4) {
-            const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
-            v0[q] = t.x; v1[q] = t.y;
-          } else {
-            const double2 t = __ldcs(reinterpret_cast<const double2*>(p));
-            v0[q] = t.x; v1[q] = t.y;
-          }
-        } else {
-          v0[q] = __ldcs(p);
-        }
-      }
-    }
-    T u0 = T(0), u1 = T(0);
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) {
-      u0 = fma_rn(v0[q], c1q[q], u0);
-      u1 = fma_rn(v1[q], c1q[q], u1);
-    }
-    u0 += __shfl_xor_sync(0xffffffffu, u0, 1);
-    u1 += __shfl_xor_sync(0xffffffffu, u1, 1);
-    u0 += __shfl_xor_sync(0xffffffffu, u0, 2);
-    u1 += __shfl_xor_sync(0xffffffffu, u1, 2);
-    const T x0 = one ? sub_rn(w[rb], u0) : T(0);
-    const T x1 = two ? sub_rn(w[rb + 1], u1) : T(0);
-    if (j == 0 && one) {
-      w[rb] = x0;
-      if (two) w[rb + 1] = x1;
-    }
-#pragma unroll
-    for (int q = 0; q < KQ; ++q) acc[q] = fma_rn(v1[q], x1, fma_rn(v0[q], x0, acc[q]));
-  }
-  // lanes with equal j hold the same vectors: reduce across quads (xor 4, 8, 16)
-#pragma unroll
-  for (int q = 0; q < KQ; ++q) {
-    T a = acc[q];
-    a += __shfl_xor_sync(0xffffffffu, a, 4);
-    a += __shfl_xor_sync(0xffffffffu, a, 8);
-    a += __shfl_xor_sync(0xffffffffu, a, 16);
-    if (lane < 4) red2[warp][4 * q + lane] = a;
-  }
-  __syncthreads();
-  T* part = static_cast<T*>(ws.part);
-  if (tid < k) {
-    T s = T(0);
-    for (int q = 0; q < kWarps; ++q) s += red2[q][tid];
-    part[(size_t)blockIdx.x * k + tid] = s;
-  }
-  if (last_cta(ws.counter)) {
-    const int jj = k - 1;
-    for (int c = warp; c < k; c += kWarps) {
-      T s2 = T(0);
-      for (int p = lane; p < (int)gridDim.x; p += 32) s2 += __ldcg(part + (size_t)p * k + c);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        if (sv.dist) { sv.red[c] = s2; continue; }   // raw local sum (distributed)
-        sv.c2[c] = s2;
-        sv.Hc(jj, c) = add_rn(add_rn(T(0), c1s[c]), s2);   // h = 0; h += c1; h += c2
       }
     }
   }
@@ -1462,44 +1285,6 @@ template <typename T>
 cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,
                                   StateView<T> sv, WsView ws, cudaStream_t st);
 
-template <typename T, int KT>
-static cudaError_t launch_update_dot_reg(const T* V, long long ldv, long long n, int k, T* w,
-                                         StateView<T> sv, WsView ws, cudaStream_t st) {
-  static std::once_flag once;
-  static int occ = 1;
-  std::call_once(once, [] {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dot_reg<T, KT>, kThreads, 0);
-    cudaGetLastError();
-    if (occ < 1) occ = 1;
-  });
-  long long G = (n + kThreads - 1) / kThreads;
-  const long long cap = (long long)num_sms() * occ;
-  if (G > cap) G = cap;
-  if (G < 1) G = 1;
-  count_launch();
-  k_update_dot_reg<T, KT><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
-  return cudaGetLastError();
-}
-
-template <typename T, int KT>
-static cudaError_t launch_update_dot_q(const T* V, long long ldv, long long n, int k, T* w,
-                                       StateView<T> sv, WsView ws, cudaStream_t st) {
-  static std::once_flag once;
-  static int occ = 1;
-  std::call_once(once, [] {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_dot_q<T, KT>, kThreads, 0);
-    cudaGetLastError();
-    if (occ < 1) occ = 1;
-  });
-  long long G = (n + 2 * (kThreads / 4) - 1) / (2 * (kThreads / 4));
-  const long long cap = (long long)num_sms() * occ;
-  if (G > cap) G = cap;
-  if (G < 1) G = 1;
-  count_launch();
-  k_update_dot_q<T, KT><<<(unsigned)G, kThreads, 0, st>>>(V, ldv, n, k, w, sv, ws);
-  return cudaGetLastError();
-}
-
 template <typename T, int KV>
 static cudaError_t launch_update_dot_w(const T* V, long long ldv, long long n, int k, T* w,
                                        StateView<T> sv, WsView ws, cudaStream_t st) {
@@ -1540,39 +1325,6 @@ cudaError_t launch_update_dot(const T* V, long long ldv, long long n, int k, T* 
     default: return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
   }
 }
-
-// kept for A/B measurement: quad-split variant
-template <typename T>
-cudaError_t launch_update_dot_quadvariant(const T* V, long long ldv, long long n, int k, T* w,
-                                          StateView<T> sv, WsView ws, cudaStream_t st) {
-  if (k <= 4) return launch_update_dot_q<T, 4>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 8) return launch_update_dot_q<T, 8>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 12) return launch_update_dot_q<T, 12>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 16) return launch_update_dot_q<T, 16>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 24) return launch_update_dot_q<T, 24>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 32) return launch_update_dot_q<T, 32>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 40) return launch_update_dot_q<T, 40>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 48) return launch_update_dot_q<T, 48>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 56) return launch_update_dot_q<T, 56>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 64) return launch_update_dot_q<T, 64>(V, ldv, n, k, w, sv, ws, st);
-  return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
-}
-
-// kept for A/B measurement (MPG kernel variant sweep): one accumulator per vector per thread
-template <typename T>
-cudaError_t launch_update_dot_regvariant(const T* V, long long ldv, long long n, int k, T* w,
-                                         StateView<T> sv, WsView ws, cudaStream_t st) {
-  if (k <= 8) return launch_update_dot_reg<T, 8>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 16) return launch_update_dot_reg<T, 16>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 32) return launch_update_dot_reg<T, 32>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 48) return launch_update_dot_reg<T, 48>(V, ldv, n, k, w, sv, ws, st);
-  if (k <= 64) return launch_update_dot_reg<T, 64>(V, ldv, n, k, w, sv, ws, st);
-  return launch_update_dot_tma<T>(V, ldv, n, k, w, sv, ws, st);
-}
-template cudaError_t launch_update_dot_regvariant<float>(const float*, long long, long long, int, float*,
-                                                         StateView<float>, WsView, cudaStream_t);
-template cudaError_t launch_update_dot_regvariant<double>(const double*, long long, long long, int, double*,
-                                                          StateView<double>, WsView, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k, T* w,
