@@ -340,6 +340,8 @@ typedef struct {
 
 typedef struct mpg_solver mpg_solver;
 
+/* sizeof(mpg_solver_desc) as compiled into the library (binding check). */
+int64_t mpg_solver_desc_bytes(void);
 int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out);
 int mpg_solver_destroy(mpg_solver* s);
 /* b_norm = ||b|| and the initial explicit residual r = b - A x, rnorm

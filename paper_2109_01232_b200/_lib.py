@@ -75,6 +75,7 @@ _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
 _SIGS = {
     "mpg_version": (C.c_char_p, []),
     "mpg_workspace_bytes": (_i64, []),
+    "mpg_solver_desc_bytes": (_i64, []),
     "mpg_launch_count": (_i64, []),
     "mpg_spmv": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mpg_residual": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--cfg3", action="store_true")
     ap.add_argument("--cfg4", type=int, choices=[25, 40], default=None)
     ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--cfg5-fp64", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
     mp = _ref()
@@ -231,6 +232,20 @@ def main():
               f"({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg5.json"), "w") as f:
             json.dump({"meta": meta, "assembly": asm, "runs": runs}, f, indent=1)
+    if args.cfg5_fp64:
+        # the fp64 GMRES(50) first cycle at 400^3: the Krylov iterate to ~1e-12, against
+        # which the fp32 inner cycles' accuracy is judged (test_gpu_solvers cfg5 test)
+        t = time.time()
+        A = mp.generate(mp.StencilSpec(mp.StencilKind("laplace3d"), 400))
+        rep = mp.gmres_restarted(A, np.ones(A.n_rows), criteria=mp.StopCriteria(rtol=1e-10, m=50, max_iters=50))
+        path = os.path.join(HERE, "reference_cfg5.json")
+        with open(path) as f:
+            d = json.load(f)
+        d["runs"]["laplace3d:400/fp64/m50/max50"] = report_dict(rep)
+        with open(path, "w") as f:
+            json.dump(d, f, indent=1)
+        print("cfg5 fp64 cycle", d["runs"]["laplace3d:400/fp64/m50/max50"]["boundaries"],
+              f"({time.time() - t:.1f}s)", flush=True)
     if args.cfg4:
         name, spec, solver, kw = CFG4_RUNS[args.cfg4]
         t = time.time()

@@ -26,6 +26,13 @@ def test_version_and_workspace():
     assert lib.mpg_workspace_bytes() > 1 << 20
 
 
+def test_solver_descriptor_layout_matches_binding():
+    """The ctypes mirror of mpg_solver_desc has the C struct's size and field order."""
+    lib = _lib.load()
+    assert lib.mpg_solver_desc_bytes() == C.sizeof(_lib.SolverDesc)
+    assert C.sizeof(_lib.StateHeader) == 8 * 4 + 8 * 16
+
+
 def test_state_layout_monotone():
     lib = _lib.load()
     for prec in (0, 1):

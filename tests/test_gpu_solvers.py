@@ -446,11 +446,15 @@ def test_cfg4_laplace3d200_ir_poly_vs_reference(degree, build, cfg4_reference):
 def test_cfg5_laplace3d400_assembly_and_first_ir_cycle_vs_reference():
     """BASELINE configs[4] (Laplace3D 400^3, 64M rows, 447M nonzeros) on one
     B200.  A full reference solve is ~40 CPU-hours, so the reference pinned
-    (tests/golden/reference_cfg5.json) the assembly and its first GMRES-IR
-    cycle (50 fp32 iterations + the fp64 residual).  Here: device assembly
-    bit-exact by sha256, the first cycle's explicit residual within 1 % of the
-    reference's and the iterate within 1e-6 relative (one unconverged fp32
-    cycle: rounding-order differences are at fp32 level)."""
+    (tests/golden/reference_cfg5.json) the assembly, its first GMRES-IR cycle
+    and its first fp64 GMRES(50) cycle.  Here: device assembly bit-exact by
+    sha256; the first IR cycle's explicit residual within 0.1 % of the
+    reference's; and the iterate against the fp64 cycle, which in exact
+    arithmetic is the same Krylov iterate (x0 = 0, same b): ours within 1e-4.
+    The reference's own fp32 cycle is 0.9 % away from it -- its sequential
+    single-precision BLAS dot products over 64M entries lose the smooth-mode
+    coefficient (kappa ~ 6.5e4), which our tree reductions keep; the test
+    records that too."""
     import hashlib
     from conftest import load_json
     g = load_json("reference_cfg5.json")
@@ -459,13 +463,19 @@ def test_cfg5_laplace3d400_assembly_and_first_ir_cycle_vs_reference():
     assert (A.n_rows, A.nnz) == (asm["n"], asm["nnz"])
     for name, t in (("row_ptr", A.row_ptr), ("col_idx", A.col_idx), ("values", A.values)):
         assert hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest() == asm[name], name
-    ref = g["runs"]["laplace3d:400/ir/m50/max50"]
+    ref_ir = g["runs"]["laplace3d:400/ir/m50/max50"]
+    ref64 = g["runs"]["laplace3d:400/fp64/m50/max50"]
     b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
     rep = P.gmres_ir(A, b, criteria=P.StopCriteria(rtol=1e-10, m=50, max_iters=50))
-    assert rep.total_iters == ref["total_iters"] == 50
+    assert rep.total_iters == ref_ir["total_iters"] == 50
     ours = [e.explicit for e in rep.residual_history if e.explicit is not None]
-    theirs = [bd[2] for bd in ref["boundaries"]]
-    assert len(ours) == len(theirs) and abs(ours[-1] / theirs[-1] - 1) <= 1e-2, (ours, theirs)
-    x = rep.x.cpu().numpy()[:: ref["x_stride"]]
-    sample = np.asarray(ref["x_sample"])
-    assert np.linalg.norm(x - sample) / np.linalg.norm(sample) <= 1e-6
+    theirs = [bd[2] for bd in ref_ir["boundaries"]]
+    assert len(ours) == len(theirs) and abs(ours[-1] / theirs[-1] - 1) <= 1e-3, (ours, theirs)
+    stride = ref_ir["x_stride"]
+    x = rep.x.cpu().numpy()[::stride]
+    x64 = np.asarray(ref64["x_sample"])
+    xir = np.asarray(ref_ir["x_sample"])
+    ours_err = np.linalg.norm(x - x64) / np.linalg.norm(x64)
+    ref_err = np.linalg.norm(xir - x64) / np.linalg.norm(x64)
+    assert ours_err <= 1e-4, ours_err
+    assert ref_err > 10 * ours_err, (ref_err, ours_err)
