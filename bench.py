@@ -232,15 +232,23 @@ def native_arm(args, rank: int, world: int):
 
     class HostCsr:  # the reference's CsrMatrix shape (numpy arrays)
         pass
+    def pinned(a):   # host inputs in page-locked memory (numpy views)
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     Ah = HostCsr()
     Ah.n_rows = Ah.n_cols = n
-    Ah.row_ptr, Ah.col_idx, Ah.values = rp, ci, v
-    bh = np.ones(n)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rep_h = gmres_ir(Ah, bh, criteria=crit)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    Ah.row_ptr, Ah.col_idx, Ah.values = pinned(rp), pinned(ci), pinned(v)
+    bh = pinned(np.ones(n))
+    # one untimed call (allocator pools, first-touch), then K timed steps; each
+    # step uploads A and b, solves, and returns x as numpy (device -> host)
+    gmres_ir(Ah, bh, criteria=crit)
+    e2e_times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep_h = gmres_ir(Ah, bh, criteria=crit)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = sum(e2e_times) / len(e2e_times)
     h2d = rp.nbytes + ci.nbytes + v.nbytes + bh.nbytes
     d2h = rep_h.x.nbytes
 
@@ -280,7 +288,10 @@ def native_arm(args, rank: int, world: int):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": {"value": round(e2e_s, 5), "unit": "s", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "iters": rep_h.total_iters},
+                "d2h_bytes_per_step": int(d2h), "iters": rep_h.total_iters,
+                "step_times_s": [round(t, 5) for t in e2e_times],
+                "note": "gmres_ir on host (pinned numpy) CSR arrays + b, x returned as numpy; "
+                        "wall clock per call, mean of the timed steps after one untimed call"},
     }
     return out
 
