@@ -12,8 +12,8 @@ CUDA events, so the batch time is device time.
 same rows (fp64 and refinement baselines plus one GMRES-FD run per switch
 point; fp64 and refinement per restart length) with ``time_s`` the solver's
 ``total_time``.  ``config`` is the reference's ``RunConfig`` (io.py:243),
-accepted duck-typed; generated problems only (Matrix Market input and RCM
-reordering are host file formats outside this path).
+accepted duck-typed; Matrix Market input and RCM reordering go through
+``paper_2109_01232_b200.io``.
 """
 
 from __future__ import annotations
@@ -29,6 +29,7 @@ import torch
 from . import _lib
 from .core import FP32, FP64, CsrMatrix, convert_matrix, ctx, ptr, stream_handle, to_device
 from .gen import generate, make_rhs
+from .io import load_matrix_market, rcm_reorder
 from .solvers import StopCriteria, gmres_fd, gmres_ir, gmres_restarted
 from .spmv import predicted_speedup
 
@@ -126,19 +127,25 @@ def spmv_bench(A, reps: int = 1000, trials: int = 3, seed: int = 0, *, warmup: i
 # sweeps (bench.py:227-312)
 
 def _problem(config):
-    if getattr(config, "matrix", None):
-        raise NotImplementedError("Matrix Market input is outside the device path (DESIGN.md §7)")
-    if getattr(config, "rcm", False):
-        raise NotImplementedError("RCM reordering is outside the device path (DESIGN.md §7)")
+    """(name, A, b) as bench.py:134-148: a Matrix Market file or a generated
+    stencil, the seeded right-hand side, optional RCM reordering."""
     if hasattr(config, "validate"):
         config.validate()
-    A = generate(config.gen)
+    if getattr(config, "matrix", None):
+        A = load_matrix_market(config.matrix)
+        name = os.path.splitext(os.path.basename(config.matrix))[0]
+    else:
+        A = generate(config.gen)
+        name = config.gen.name
     rhs = config.rhs
     if getattr(rhs, "seed", None) != config.seed:
         from dataclasses import replace
         rhs = replace(rhs, seed=config.seed)
     b = make_rhs(rhs, A.n_rows)
-    return config.gen.name, A, b
+    if getattr(config, "rcm", False):
+        perm, A = rcm_reorder(A)
+        b = perm.apply(b)
+    return name, A, b
 
 
 def _write_rows(rows: list[dict], fields: list[str], path: str) -> None:

@@ -169,12 +169,71 @@ def spmv_fixtures(mp):
     return out
 
 
+def io_fixtures(mp, meta):
+    """Matrix Market files (written here as text) loaded by the reference, and
+    its reverse Cuthill-McKee permutations (io.py:59-121, precond.py:421-515)."""
+    from mpgmres import io as mio
+    from mpgmres import precond as mpc
+    rng = np.random.default_rng(7)
+    d = os.path.join(HERE, "mm")
+    os.makedirs(d, exist_ok=True)
+    files = {}
+    # general real with duplicates (summed) and comments
+    n = 40
+    r = rng.integers(1, n + 1, 300); c = rng.integers(1, n + 1, 300); v = rng.standard_normal(300)
+    lines = ["%%MatrixMarket matrix coordinate real general", "% a comment", f"{n} {n} 300"]
+    lines += [f"{a} {b} {x:.17g}" for a, b, x in zip(r, c, v)]
+    files["general_dups.mtx"] = "\n".join(lines) + "\n"
+    # symmetric (lower triangle stored, diagonal once)
+    ent = {(i, i): 4.0 + i for i in range(1, 31)}
+    for _ in range(80):
+        a, b = sorted(rng.integers(1, 31, 2))
+        if a != b:
+            ent[(b, a)] = float(rng.standard_normal())
+    lines = ["%%MatrixMarket matrix coordinate real symmetric", f"30 30 {len(ent)}"]
+    lines += [f"{a} {b} {x:.17g}" for (a, b), x in ent.items()]
+    files["symmetric.mtx"] = "\n".join(lines) + "\n"
+    # integer field, rectangular
+    lines = ["%%MatrixMarket matrix coordinate integer general", "5 7 6",
+             "1 1 3", "2 7 -1", "5 2 8", "3 3 1", "4 6 2", "1 1 4"]
+    files["integer_rect.mtx"] = "\n".join(lines) + "\n"
+    out = {"meta": meta, "mm": {}, "rcm": {}}
+    for name, text in files.items():
+        path = os.path.join(d, name)
+        with open(path, "w") as f:
+            f.write(text)
+        A = mio.load_matrix_market(path)
+        out["mm"][name] = {"n_rows": A.n_rows, "n_cols": A.n_cols, "nnz": A.nnz, "row_ptr": sha(A.row_ptr),
+                           "col_idx": sha(A.col_idx), "values": sha(A.values)}
+    # RCM permutations
+    mats = {"laplace2d:12": mp.generate(mp.StencilSpec(mp.StencilKind("laplace2d"), 12)),
+            "convdiff2d:9": mp.generate(mp.StencilSpec(mp.StencilKind("convdiff2d"), 9, convection=3.0)),
+            "symmetric.mtx": mio.load_matrix_market(os.path.join(d, "symmetric.mtx")),
+            "general_dups.mtx": mio.load_matrix_market(os.path.join(d, "general_dups.mtx"))}
+    # a shuffled stencil (RCM recovers a banded order) and a disconnected block matrix
+    L = mats["laplace2d:12"]
+    p = rng.permutation(L.n_rows)
+    mats["laplace2d:12:shuffled"] = mpc.permute_csr(L, mpc.Permutation(p))
+    blk = np.zeros((12, 12)); blk[:5, :5] = rng.standard_normal((5, 5)); blk[7:, 7:] = rng.standard_normal((5, 5))
+    blk[5, 5] = blk[6, 6] = 1.0
+    mats["blocks12"] = mp.CsrMatrix.from_dense(blk)
+    for name, A in mats.items():
+        perm, B = mpc.rcm_reorder(A)
+        out["rcm"][name] = {"n": A.n_rows, "row_ptr": A.row_ptr.tolist(), "col_idx": A.col_idx.tolist(),
+                            "perm": perm.perm.tolist(), "permuted_row_ptr": sha(B.row_ptr),
+                            "permuted_col_idx": sha(B.col_idx), "permuted_values": sha(B.values),
+                            "values": A.values.tolist()}
+    with open(os.path.join(HERE, "reference_io.json"), "w") as f:
+        json.dump(out, f)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
     ap.add_argument("--cfg3", action="store_true")
     ap.add_argument("--cfg4", type=int, choices=[25, 40], default=None)
     ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--io", action="store_true")
     ap.add_argument("--cfg5-fp64", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
@@ -232,6 +291,8 @@ def main():
               f"({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg5.json"), "w") as f:
             json.dump({"meta": meta, "assembly": asm, "runs": runs}, f, indent=1)
+    if args.io:
+        io_fixtures(mp, meta)
     if args.cfg5_fp64:
         # the fp64 GMRES(50) first cycle at 400^3: the Krylov iterate to ~1e-12, against
         # which the fp32 inner cycles' accuracy is judged (test_gpu_solvers cfg5 test)
