@@ -29,12 +29,12 @@ import torch
 from . import _lib
 from .core import FP32, FP64, CsrMatrix, convert_matrix, ctx, ptr, stream_handle, to_device
 from .gen import generate, make_rhs
-from .io import load_matrix_market, rcm_reorder
+from .io import load_matrix_market, rcm_reorder, write_convergence_csv, write_summary_csv
 from .solvers import StopCriteria, gmres_fd, gmres_ir, gmres_restarted
 from .spmv import predicted_speedup
 
-__all__ = ["Quadrant", "SpmvBenchResult", "classify_speedup", "spmv_bench", "sweep_switch_point",
-           "sweep_restart", "SWITCH_FIELDS", "RESTART_FIELDS"]
+__all__ = ["Quadrant", "SpmvBenchResult", "classify_speedup", "spmv_bench", "run_experiment", "summary_row",
+           "sweep_switch_point", "sweep_restart", "SWITCH_FIELDS", "RESTART_FIELDS"]
 
 MAX_ROW_NNZ_THRESHOLD = 15      # bench.py:42
 SPEEDUP_THRESHOLD = 1.7         # bench.py:43
@@ -126,9 +126,9 @@ def spmv_bench(A, reps: int = 1000, trials: int = 3, seed: int = 0, *, warmup: i
 # ---------------------------------------------------------------------------
 # sweeps (bench.py:227-312)
 
-def _problem(config):
-    """(name, A, b) as bench.py:134-148: a Matrix Market file or a generated
-    stencil, the seeded right-hand side, optional RCM reordering."""
+def _problem(config, keep_perm: bool = False):
+    """(name, A, b[, perm]) as bench.py:134-148: a Matrix Market file or a
+    generated stencil, the seeded right-hand side, optional RCM reordering."""
     if hasattr(config, "validate"):
         config.validate()
     if getattr(config, "matrix", None):
@@ -142,10 +142,70 @@ def _problem(config):
         from dataclasses import replace
         rhs = replace(rhs, seed=config.seed)
     b = make_rhs(rhs, A.n_rows)
+    perm = None
     if getattr(config, "rcm", False):
         perm, A = rcm_reorder(A)
         b = perm.apply(b)
-    return name, A, b
+    return (name, A, b, perm) if keep_perm else (name, A, b)
+
+
+def _precond(config, A, precision):
+    """bench.py:151-158: none, jacobi:K or poly:D built on A in `precision`."""
+    from .precond import build_block_jacobi, build_poly_precond
+    spec = config.precond
+    if spec.kind == "none":
+        return None
+    At = A if A.precision is precision else convert_matrix(A, precision)
+    if spec.kind == "poly":
+        return build_poly_precond(At, spec.param, seed=config.seed)
+    return build_block_jacobi(At, spec.param)
+
+
+def _solve_once(config, A, b, perm=None):
+    """bench.py:165-188: the configured solver on (A, b)."""
+    criteria = StopCriteria(rtol=config.rtol, max_iters=config.max_iters, m=config.m)
+    kind = config.solver.value if hasattr(config.solver, "value") else str(config.solver)
+    if kind == "double":
+        pc = _precond(config, A, FP32 if getattr(config, "precond_fp32", False) else FP64)
+        rep = gmres_restarted(A, b, criteria=criteria, precond=pc, precision=FP64)
+    elif kind == "single":
+        rep = gmres_restarted(A, b, criteria=criteria, precond=_precond(config, A, FP32), precision=FP32)
+    elif kind == "ir":
+        rep = gmres_ir(A, b, criteria=criteria, precond_fp32=_precond(config, A, FP32))
+    elif kind == "fd":
+        if config.precond.kind != "none":
+            raise ValueError("the precision-switching solver does not take a preconditioner")
+        rep = gmres_fd(A, b, criteria=criteria, switch_iter=config.switch_iter)
+    else:
+        raise ValueError(f"unknown solver {kind}")
+    if perm is not None:
+        rep.x = perm.invert_apply(rep.x)
+    return rep
+
+
+def summary_row(name: str, A, config, report) -> dict:
+    """bench.py:213-224."""
+    kind = config.solver.value if hasattr(config.solver, "value") else str(config.solver)
+    return {"name": name, "n": A.n_rows, "nnz": A.nnz, "solver": kind, "precond": str(config.precond),
+            "time_s": repr(report.total_time), "iters": report.total_iters, "converged": report.converged,
+            "loss_of_accuracy": report.loss_of_accuracy}
+
+
+def run_experiment(config, out_dir: str | None = None, repeats: int = 3):
+    """Run the configured solver ``repeats`` times and keep the median-time run,
+    writing the convergence history and a one-row summary CSV when an output
+    directory is given (bench.py:191-210)."""
+    name, A, b, perm = _problem(config, keep_perm=True)
+    reports = sorted((_solve_once(config, A, b, perm) for _ in range(repeats)), key=lambda r: r.total_time)
+    report = reports[len(reports) // 2]
+    out = out_dir or getattr(config, "out", None)
+    if out:
+        os.makedirs(out, exist_ok=True)
+        kind = config.solver.value if hasattr(config.solver, "value") else str(config.solver)
+        tag = f"{name.replace(':', '_')}_{kind}"
+        write_convergence_csv(report, os.path.join(out, f"convergence_{tag}.csv"))
+        write_summary_csv([summary_row(name, A, config, report)], os.path.join(out, f"summary_{tag}.csv"))
+    return report
 
 
 def _write_rows(rows: list[dict], fields: list[str], path: str) -> None:

@@ -19,13 +19,15 @@ are what the CPU tests pin against the reference's outputs.
 
 from __future__ import annotations
 
+import csv
 from collections import deque
 from dataclasses import dataclass
 
 import numpy as np
 
 __all__ = ["MatrixMarketError", "load_matrix_market", "write_matrix_market", "read_matrix_market_arrays",
-           "Permutation", "rcm_order", "rcm_reorder", "permute_csr"]
+           "Permutation", "rcm_order", "rcm_reorder", "permute_csr", "write_convergence_csv",
+           "read_convergence_csv", "write_summary_csv", "SUMMARY_FIELDS"]
 
 
 class MatrixMarketError(ValueError):
@@ -221,3 +223,33 @@ def rcm_reorder(A):
         raise ShapeError("reordering needs a square matrix")
     perm = Permutation(rcm_order(A.n_rows, A.row_ptr.cpu().numpy(), A.col_idx.cpu().numpy()))
     return perm, permute_csr(A, perm)
+
+
+# ---------------------------------------------------------------------------
+# result CSVs (io.py:165-201): the same artefacts the reference writes
+
+def write_convergence_csv(report, path) -> None:
+    """Per-iteration residual history; explicit entries blank off the restart boundaries."""
+    with open(path, "w", encoding="utf-8", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["iteration", "implicit_relres", "explicit_relres", "phase"])
+        w.writerows([e.iteration, repr(e.implicit), "" if e.explicit is None else repr(e.explicit), e.phase]
+                    for e in report.residual_history)
+
+
+def read_convergence_csv(path) -> list:
+    from .solvers import HistoryEntry
+    with open(path, "r", encoding="utf-8", newline="") as fh:
+        rows = list(csv.reader(fh))[1:]
+    return [HistoryEntry(int(r[0]), float(r[1]), None if r[2] == "" else float(r[2]), r[3]) for r in rows]
+
+
+SUMMARY_FIELDS = ["name", "n", "nnz", "solver", "precond", "time_s", "iters", "converged", "loss_of_accuracy"]
+
+
+def write_summary_csv(rows: list[dict], path) -> None:
+    """Solver-comparison summary, one solve per row."""
+    with open(path, "w", encoding="utf-8", newline="") as fh:
+        w = csv.DictWriter(fh, fieldnames=SUMMARY_FIELDS)
+        w.writeheader()
+        w.writerows({k: row.get(k, "") for k in SUMMARY_FIELDS} for row in rows)

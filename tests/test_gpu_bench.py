@@ -84,3 +84,20 @@ def test_matrix_market_and_rcm_device_path(tmp_path):
 
 
 B_ = B
+
+
+def test_run_experiment_median_and_csv_artefacts(tmp_path):
+    """run_experiment (bench.py:191-210): median-time run of `repeats`, the
+    convergence and summary CSVs the reference writes (io.py:165-201)."""
+    from types import SimpleNamespace
+    from paper_2109_01232_b200 import io as mio
+    cfg = _config("laplace2d", 50)
+    cfg.solver = SimpleNamespace(value="ir")
+    cfg.precond = SimpleNamespace(kind="jacobi", param=1, __str__=lambda self: "jacobi:1")
+    cfg.precond_fp32, cfg.switch_iter = False, 0
+    rep = B.run_experiment(cfg, out_dir=str(tmp_path), repeats=3)
+    assert rep.converged and rep.total_iters == 250          # reference: laplace2d:50 IR = 250
+    hist = mio.read_convergence_csv(str(tmp_path / "convergence_laplace2d_50_ir.csv"))
+    assert hist == rep.residual_history
+    text = (tmp_path / "summary_laplace2d_50_ir.csv").read_text().splitlines()
+    assert text[0].split(",") == mio.SUMMARY_FIELDS and ",250,True,False" in text[1]
