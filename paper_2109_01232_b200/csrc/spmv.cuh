@@ -296,11 +296,21 @@ __device__ __forceinline__ void stencil_loop(long long n, E& epi, EpiShared<T>& 
     const int nrows = (int)min((long long)kSpTile, n - a);
     T* ys = es.ys[t & 1];
     for (int rr = threadIdx.x; rr < nrows; rr += kSpConsumers) ys[rr] = epi.on_row(a + rr, rowf(a + rr));
-    consumer_sync();
-    epi.on_tile(a, nrows, ys);
+    if constexpr (needs_tiles<E>::value) {
+      consumer_sync();
+      epi.on_tile(a, nrows, ys);
+    }
   }
   epi.on_end();
 }
+
+// Epilogues with a per-tile hook (on_tile reads the tile's results from shared
+// memory: the fused K_A dots) declare kNeedsTiles; the others skip the
+// per-tile barrier.
+template <typename E, typename = void> struct needs_tiles { static constexpr bool value = false; };
+template <typename E> struct needs_tiles<E, decltype((void)E::kNeedsTiles)> {
+  static constexpr bool value = E::kNeedsTiles;
+};
 
 // Epilogues may take a whole 16-byte row group at once (kVecRows + on_rows);
 // otherwise the group is handed over row by row.
@@ -414,8 +424,10 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
       stencil_group<T, S>(SV, x, r0, off, mis, y);
       epi_rows(epi, r0, y, min(VN, nrows - rr), ys + rr);
     }
-    consumer_sync();
-    epi.on_tile(a, nrows, ys);
+    if constexpr (needs_tiles<E>::value) {
+      consumer_sync();
+      epi.on_tile(a, nrows, ys);
+    }
   }
   epi.on_end();
 }

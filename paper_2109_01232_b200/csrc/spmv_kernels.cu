@@ -446,10 +446,6 @@ constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
 constexpr int kCsrCap = 384;   // staged nonzeros per warp chunk (avg <= 12 per row)
 
-template <typename E, typename = void> struct needs_tiles { static constexpr bool value = false; };
-template <typename E> struct needs_tiles<E, decltype((void)E::kNeedsTiles)> {
-  static constexpr bool value = E::kNeedsTiles;
-};
 
 template <typename T, typename E>
 __global__ void __launch_bounds__(kCsrThreads) k_csr_warp(CsrView<T> A, const T* __restrict__ x, E epi) {
