@@ -239,7 +239,9 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   T* wbuf[2] = {w, fuse ? static_cast<T*>(d.u) : w};
   // single-GPU stencil storage without a preconditioner: one persistent
   // cooperative kernel per Arnoldi step (step_kernel.cu) when it applies
-  const bool mega_ok = !fuse && d.pc_kind == MPG_PC_NONE && !d.dist && d.stencil_dims && d.dia &&
+  // Jacobi(1) in the working precision rides along: the step kernel also writes z = v / diag
+  const bool jac1 = d.pc_kind == MPG_PC_JACOBI && d.pc_block == 1 && d.pc_prec == d.prec;
+  const bool mega_ok = !fuse && (d.pc_kind == MPG_PC_NONE || jac1) && !d.dist && d.stencil_dims && d.dia &&
                        d.halo >= (d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx
                                                       : (long long)d.stencil_nx);
   int sk = d.step_kernel;
@@ -248,11 +250,23 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
   for (int j = 0; j < m_limit; ++j) {
     T* wj = wbuf[j & 1];
     if (mega && j + 1 <= kMegaMaxK) {
+      const T* xin = V + (size_t)j * d.ldv;
+      T* zbuf = jac1 ? static_cast<T*>(d.pc_t0) : nullptr;
+      // Jacobi: z_0 comes from the apply kernel; later z_j from the previous step kernel
+      if (jac1 && (j == 0 || j > kMegaMaxK)) {
+        ProfScope pp(PK_PRECOND);
+        const T* z = nullptr;
+        TRY(precond_apply<T>(s, xin, &z, ws, h, st));
+      }
       ProfScope ps(PK_STEP);
       StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
                        d.stencil_dims, d.row0};
       S.padded = 1;
-      TRY(launch_step_mega<T>(S, V + (size_t)j * d.ldv, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st));
+      // the last persistent step hands the four-launch steps V[:, j+1]; they apply M themselves
+      const bool next_mega = j + 2 <= kMegaMaxK && j + 1 < m_limit;
+      TRY(launch_step_mega<T>(S, jac1 ? zbuf : xin, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st,
+                              jac1 && next_mega ? static_cast<const T*>(d.pc_lu) : nullptr,
+                              jac1 && next_mega ? zbuf : nullptr));
       continue;
     }
     if (fuse && j > 0) {

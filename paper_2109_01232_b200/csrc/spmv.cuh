@@ -58,6 +58,14 @@ struct alignas(16) EpiShared {
   T acc[8];
 };
 
+// Epilogues with a per-tile hook (on_tile reads the tile's results from shared
+// memory: the fused K_A dots) declare kNeedsTiles; the others skip the
+// per-tile barrier.
+template <typename E, typename = void> struct needs_tiles { static constexpr bool value = false; };
+template <typename E> struct needs_tiles<E, decltype((void)E::kNeedsTiles)> {
+  static constexpr bool value = E::kNeedsTiles;
+};
+
 template <typename T>
 struct alignas(128) SpSmem {
   alignas(16) int32_t rp[kSpStages][kSpTile + 8];
@@ -303,14 +311,6 @@ __device__ __forceinline__ void stencil_loop(long long n, E& epi, EpiShared<T>& 
   }
   epi.on_end();
 }
-
-// Epilogues with a per-tile hook (on_tile reads the tile's results from shared
-// memory: the fused K_A dots) declare kNeedsTiles; the others skip the
-// per-tile barrier.
-template <typename E, typename = void> struct needs_tiles { static constexpr bool value = false; };
-template <typename E> struct needs_tiles<E, decltype((void)E::kNeedsTiles)> {
-  static constexpr bool value = E::kNeedsTiles;
-};
 
 // Epilogues may take a whole 16-byte row group at once (kVecRows + on_rows);
 // otherwise the group is handed over row by row.

@@ -164,9 +164,12 @@ cudaError_t launch_halo_wait(mpg_state_header* h, const uint32_t* flags, int has
 // persistent per-step kernel (step_kernel.cu), stencil storage, single GPU;
 // steps with k > kMegaMaxK basis vectors use the four-launch step
 constexpr int kMegaMaxK = 56;
+// jdiag / zout: Jacobi(1) right preconditioning -- the kernel also writes the
+// next step's operator input z = V[:, j+1] / diag (x is then z_j, not V[:, j])
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& S, const T* x, T* V, long long ldv, long long n, int j,
-                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st);
+                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
+                             const T* jdiag = nullptr, T* zout = nullptr);
 int mega_env();   // MPG_MEGA: 1 / 0 forces the persistent / four-launch step, -1 unset
 
 // distributed-mode post phases (k_dist_post)

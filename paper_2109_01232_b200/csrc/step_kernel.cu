@@ -61,7 +61,7 @@ __device__ __forceinline__ T sum_column(const T* part, int col, int G) {
 template <typename T, int S, int KV, bool CACHE>
 __global__ void __launch_bounds__(kMegaThreads, 1)
 k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
-            T* wg, StateView<T> sv, WsView ws, int m_limit) {
+            T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout) {
   if (gated(sv.h)) return;
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
@@ -352,6 +352,17 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
 #pragma unroll
     for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);   // rows >= n stay 0
     vstore(vn + r, a);
+    if (jdiag) {   // Jacobi(1): the next step's operator input z = v / diag (precond.py:384-390)
+      if (r + VN <= n) {
+        T dv[VN];
+        vload(jdiag + r, dv);
+#pragma unroll
+        for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], dv[e]);
+        vstore(zout + r, a);
+      } else {
+        for (int e = 0; r + e < n; ++e) zout[r + e] = div_rn(a[e], __ldg(jdiag + r + e));
+      }
+    }
   }
 }
 
@@ -377,7 +388,7 @@ int mega_env() {
 template <typename T, int S, int KV, bool CACHE>
 static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
-                                 unsigned grid, size_t smem) {
+                                 unsigned grid, size_t smem, const T* jdiag, T* zout) {
   static std::once_flag once;
   std::call_once(once, [] {
     int dev = 0, optin = 0;
@@ -389,12 +400,13 @@ static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, lon
   });
   count_launch();
   return launch_k(false, true, k_step_mega<T, S, KV, CACHE>, dim3(grid), dim3(kMegaThreads), smem, st, SV, x,
-                  V, ldv, n, j, w, sv, ws, m_limit);
+                  V, ldv, n, j, w, sv, ws, m_limit, jdiag, zout);
 }
 
 template <typename T, int S, int KV>
 static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
-                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
+                                  const T* jdiag, T* zout) {
   constexpr int RB = 32 * Vec<T>::n;
   const long long nblk = (n + RB - 1) / RB;
   const long long G = std::min<long long>(num_sms(), nblk);
@@ -408,20 +420,23 @@ static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, lo
   // static shared memory of the kernel (upart, xs, column scratch) + headroom
   const size_t stat = sizeof(T) * (kMegaGroups * 9 * RB + 3 * kMegaMaxCols * 2) + 2048;
   if (cache + stat <= (size_t)optin)
-    return launch_mega_k<T, S, KV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache);
-  return launch_mega_k<T, S, KV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0);
+    return launch_mega_k<T, S, KV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache, jdiag,
+                                         zout);
+  return launch_mega_k<T, S, KV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0, jdiag, zout);
 }
 
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n, int j,
-                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st) {
+                             T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st, const T* jdiag,
+                             T* zout) {
   const int k = j + 1;
   if (k > kMegaMaxK || k + 2 > kMegaMaxCols || !SV.padded || SV.xdiv) return cudaErrorInvalidValue;
   const int kv = (k + 7) / 8;
 #define MEGA_CASE(KVV)                                                                            \
   case KVV:                                                                                       \
-    return SV.dims == 3 ? launch_mega_kv<T, 7, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st)  \
-                        : launch_mega_kv<T, 5, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st);
+    return SV.dims == 3                                                                           \
+               ? launch_mega_kv<T, 7, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout)  \
+               : launch_mega_kv<T, 5, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout);
   switch (kv) {
     MEGA_CASE(1)
     MEGA_CASE(2)
@@ -438,9 +453,9 @@ cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long lo
 
 template cudaError_t launch_step_mega<float>(const StencilView<float>&, const float*, float*, long long,
                                              long long, int, float*, StateView<float>, WsView, int,
-                                             cudaStream_t);
+                                             cudaStream_t, const float*, float*);
 template cudaError_t launch_step_mega<double>(const StencilView<double>&, const double*, double*, long long,
                                               long long, int, double*, StateView<double>, WsView, int,
-                                              cudaStream_t);
+                                              cudaStream_t, const double*, double*);
 
 }  // namespace mpg

@@ -233,6 +233,7 @@ def main():
     ap.add_argument("--cfg3", action="store_true")
     ap.add_argument("--cfg4", type=int, choices=[25, 40], default=None)
     ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--cfg2-fd", type=int, default=None, metavar="SWITCH")
     ap.add_argument("--io", action="store_true")
     ap.add_argument("--cfg5-fp64", action="store_true")
     ap.add_argument("--skip-small", action="store_true")
@@ -291,6 +292,18 @@ def main():
               f"({time.time() - t:.1f}s)", flush=True)
         with open(os.path.join(HERE, "reference_cfg5.json"), "w") as f:
             json.dump({"meta": meta, "assembly": asm, "runs": runs}, f, indent=1)
+    if args.cfg2_fd is not None:
+        # BASELINE configs[1] lists GMRES-FD beside fp64 and IR: one switch point
+        name = f"laplace3d:150/fd{args.cfg2_fd}/m50"
+        t = time.time()
+        rep = run_one(mp, ("laplace3d", 150, {}), "fd", {"m": 50, "switch_iter": args.cfg2_fd})
+        path = os.path.join(HERE, "reference_cfg2.json")
+        with open(path) as f:
+            d = json.load(f)
+        d["runs"][name] = report_dict(rep)
+        with open(path, "w") as f:
+            json.dump(d, f, indent=1)
+        print(f"{name}: {rep.total_iters} it ({time.time() - t:.1f}s)", flush=True)
     if args.io:
         io_fixtures(mp, meta)
     if args.cfg5_fp64:

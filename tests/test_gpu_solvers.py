@@ -289,9 +289,13 @@ def test_stencil_storage_with_preconditioners():
     Ao = O.stencil_csr("laplace3d", 16)
     A, b = dev(Ao), np.ones(Ao.n_rows)
     for M in (O.poly_build(Ao.astype(np.float32), 12, seed=0), O.jacobi_build(Ao.astype(np.float32), 1)):
-        r1 = P.gmres_ir(A, b, precond_fp32=M, storage="csr")
-        r2 = P.gmres_ir(A, b, precond_fp32=M, storage="stencil")
+        with P.solvers.step_kernel("split"):
+            r1 = P.gmres_ir(A, b, precond_fp32=M, storage="csr")
+            r2 = P.gmres_ir(A, b, precond_fp32=M, storage="stencil")
         assert r1.total_iters == r2.total_iters and np.array_equal(r1.x, r2.x)
+        # the persistent step (Jacobi(1) folded into its scaling phase) agrees to rounding
+        r3 = P.gmres_ir(A, b, precond_fp32=M, storage="stencil")
+        assert abs(r3.total_iters - r1.total_iters) <= 1 and np.linalg.norm(r3.x - r1.x) <= 1e-9 * np.linalg.norm(r1.x)
 
 
 @pytest.fixture(scope="module")
