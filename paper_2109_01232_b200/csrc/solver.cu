@@ -230,30 +230,23 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
     TRY(launch_start_scale<T>(static_cast<const T*>(d.r), V, d.n, sv, st));
   }
   }
-  // Without a preconditioner the basis scaling V[:, j] = w / h_sub (krylov.py:148)
-  // is folded into step j's SpMV: it gathers w / h with the same IEEE division
-  // and writes V[:, j] for its own rows, so w ping-pongs between two buffers.
-  // Measured on B200 (cfg2): the 7 IEEE divisions per row cost more than the separate
-  // 10 us scaling launch saves, so the fused variant stays off (kept for A/B runs).
-  const bool fuse = false && d.pc_kind == MPG_PC_NONE && d.m <= 64;
-  T* wbuf[2] = {w, fuse ? static_cast<T*>(d.u) : w};
-  // single-GPU stencil storage without a preconditioner: one persistent
-  // cooperative kernel per Arnoldi step (step_kernel.cu) when it applies
-  // Jacobi(1) in the working precision rides along: the step kernel also writes z = v / diag
+  // single-GPU stencil storage, unpreconditioned or Jacobi(1) in the working
+  // precision: one persistent cooperative kernel per Arnoldi step
+  // (step_kernel.cu; for Jacobi(1) it also writes the next z = v / diag)
   const bool jac1 = d.pc_kind == MPG_PC_JACOBI && d.pc_block == 1 && d.pc_prec == d.prec;
-  const bool mega_ok = !fuse && (d.pc_kind == MPG_PC_NONE || jac1) && !d.dist && d.stencil_dims && d.dia &&
+  const bool mega_ok = (d.pc_kind == MPG_PC_NONE || jac1) && !d.dist && d.stencil_dims && d.dia &&
                        d.halo >= (d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx
                                                       : (long long)d.stencil_nx);
   int sk = d.step_kernel;
   if (mega_env() >= 0) sk = mega_env() ? 2 : 1;
   const bool mega = mega_ok && (sk == 2 || (sk == 0 && (double)d.n * sizeof(T) <= 20e6));
   for (int j = 0; j < m_limit; ++j) {
-    T* wj = wbuf[j & 1];
+    T* const wj = w;
     if (mega && j + 1 <= kMegaMaxK) {
       const T* xin = V + (size_t)j * d.ldv;
       T* zbuf = jac1 ? static_cast<T*>(d.pc_t0) : nullptr;
       // Jacobi: z_0 comes from the apply kernel; later z_j from the previous step kernel
-      if (jac1 && (j == 0 || j > kMegaMaxK)) {
+      if (jac1 && j == 0) {
         ProfScope pp(PK_PRECOND);
         const T* z = nullptr;
         TRY(precond_apply<T>(s, xin, &z, ws, h, st));
@@ -269,39 +262,30 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
                               jac1 && next_mega ? zbuf : nullptr));
       continue;
     }
-    if (fuse && j > 0) {
-      ProfScope ps(PK_SPMV_DOT);
-      const T* hprev = sv.H + (size_t)(j - 1) * (d.m + 1) + j;   // H[j, j-1] = h_sub of step j-1
-      TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
-        return launch_spmv_dot1<T>(A, wbuf[(j - 1) & 1], wj, V, d.ldv, j + 1, sv, ws, st, hprev,
-                                   V + (size_t)j * d.ldv);
-      }));
-    } else {
-      const T* vj = V + (size_t)j * d.ldv;
-      const T* z = nullptr;
-      { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
-      if (split_spmv_dot1()) {
-        {
-          ProfScope ps(PK_SPMV_DOT);
-          TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
-        }
-        ProfScope ps(PK_DOT1);
-        TRY(launch_dot1_wo<T>(wj, d.n, V, d.ldv, j + 1, sv, ws, st));
-      } else {
+    const T* vj = V + (size_t)j * d.ldv;
+    const T* z = nullptr;
+    { ProfScope ps(PK_PRECOND); TRY(precond_apply<T>(s, vj, &z, ws, h, st)); }
+    if (split_spmv_dot1()) {
+      {
         ProfScope ps(PK_SPMV_DOT);
-        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
-          return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
-        }));
+        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
       }
+      ProfScope ps(PK_DOT1);
+      TRY(launch_dot1_wo<T>(wj, d.n, V, d.ldv, j + 1, sv, ws, st));
+    } else {
+      ProfScope ps(PK_SPMV_DOT);
+      TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) {
+        return launch_spmv_dot1<T>(A, z, wj, V, d.ldv, j + 1, sv, ws, st);
+      }));
     }
     { ProfScope ps(PK_UPDATE_DOT); TRY(launch_update_dot<T>(V, d.ldv, d.n, j + 1, wj, sv, ws, st)); }
-    if (fuse_update_norm_scale() && !fuse) {
+    if (fuse_update_norm_scale()) {
       ProfScope ps(PK_UPDATE_NORM);
       TRY(launch_update_norm_scale<T>(V, d.ldv, d.n, j, wj, sv, ws, m_limit, st));
       continue;
     }
     { ProfScope ps(PK_UPDATE_NORM); TRY(launch_update_norm<T>(V, d.ldv, d.n, j, wj, sv, ws, m_limit, st)); }
-    if (!fuse) {
+    {
       ProfScope ps(PK_SCALE);
       TRY(launch_step_scale<T>(wj, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st));
     }

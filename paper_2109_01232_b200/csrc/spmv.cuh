@@ -35,16 +35,7 @@ struct CsrView {
   const int32_t* ci;
   const T* v;
   long long n;
-  // fused basis scaling (stencil path only; see StencilView)
-  const T* xdiv = nullptr;
 };
-
-// x_c, or x_c / h when the SpMV consumes an unscaled basis vector
-template <typename T>
-__device__ __forceinline__ T xload(const T* __restrict__ x, long long c, bool scaled, T h) {
-  const T v = __ldg(x + c);
-  return scaled ? div_rn(v, h) : v;
-}
 
 // largest tile any pipeline hands to an epilogue (the vectorised stencil loop:
 // kSpConsumers threads x one 16-byte row group)
@@ -170,7 +161,6 @@ struct StencilView {
   int nx;
   int dims;
   long long row0;
-  const T* xdiv = nullptr;   // fused basis scaling (see CsrView)
   // 1: every SpMV input has >= one grid plane of readable padding (or halo)
   // on both sides, so rows use the branchless sentinel path below
   int padded = 0;
@@ -201,35 +191,6 @@ template <> __host__ __device__ inline double absent_value<double>() {
 #endif
 }
 
-// Branchless row on padded inputs: all S value loads and S neighbour loads
-// are unconditional (absent slots read padding / the sentinel), then the
-// add.reduceat order p0 + (((p1 + p2) + p3) ...) over the present slots is
-// applied with selects.  No grid coordinates are needed.
-template <typename T, int S, bool scaled>
-__device__ __forceinline__ T stencil_row_padded(const T* __restrict__ v, size_t ld,
-                                                const T* __restrict__ xr, const long long (&off)[S],
-                                                T hdiv) {
-  T pv[S], px[S];
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    pv[s] = __ldg(v + s * ld);
-    px[s] = __ldg(xr + off[s]);
-  }
-  bool have = false;
-  T p0 = T(0), rest = T(-0.0);
-#pragma unroll
-  for (int s = 0; s < S; ++s) {
-    const T xs = scaled ? div_rn(px[s], hdiv) : px[s];
-    const T p = mul_rn(pv[s], xs);
-    const bool pr = present(pv[s]);
-    const T nrest = add_rn(rest, p);
-    rest = (pr && have) ? nrest : rest;
-    p0 = (pr && !have) ? p : p0;
-    have = have || pr;
-  }
-  return add_rn(p0, rest);
-}
-
 // exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
 __device__ __forceinline__ unsigned div_nx(unsigned r, unsigned long long magic) {
   return (unsigned)(((unsigned long long)r * magic) >> 48);
@@ -255,9 +216,8 @@ __device__ __forceinline__ T stencil_reduce(const bool (&pr)[S], const T (&pv)[S
   return add_rn(p0, rest);
 }
 
-template <typename T, bool scaled = false>
-__device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __restrict__ x,
-                                         long long r, T hdiv = T(1)) {
+template <typename T>
+__device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __restrict__ x, long long r) {
   const unsigned nx = (unsigned)S.nx;
   const unsigned long long mg = nx_magic(nx);
   const unsigned ur = (unsigned)(r + S.row0);
@@ -276,7 +236,7 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
 #pragma unroll
     for (int s = 0; s < 7; ++s) {
       pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
-      px[s] = pr[s] ? (scaled ? div_rn(__ldg(x + r + off[s]), hdiv) : __ldg(x + r + off[s])) : T(0);
+      px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
     }
     return stencil_reduce<T, 7>(pr, pv, px);
   }
@@ -286,7 +246,7 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
 #pragma unroll
   for (int s = 0; s < 5; ++s) {
     pv[s] = pr[s] ? __ldg(v + s * ld) : T(0);
-    px[s] = pr[s] ? (scaled ? div_rn(__ldg(x + r + off[s]), hdiv) : __ldg(x + r + off[s])) : T(0);
+    px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
   }
   return stencil_reduce<T, 5>(pr, pv, px);
 }
@@ -343,18 +303,14 @@ __device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)
   }
 }
 
-// Vectorised branchless stencil rows on padded inputs: each consumer thread
-// owns one 16-byte group of VN consecutive rows.  Per group: S 16-byte value
-// loads (slot-major storage is VN-aligned), one 16-byte load of x[r0..] that
-// also feeds the +-1 neighbours (plus one scalar each), and one window load
-// per +-nx / +-nx^2 neighbour (16-byte when aligned).  The per-row reduction is
-// stencil_row_padded's: add.reduceat order over the present slots, bit-exact.
 // One 16-byte group of VN consecutive rows r0.. (r0 % VN == 0) on padded
 // inputs: S 16-byte value loads (slot-major storage is VN-aligned), one 16-byte
 // load of x[r0..] that also feeds the +-1 neighbours (plus one scalar each),
-// one window load per +-nx / +-nx^2 neighbour (16-byte when aligned).  The
-// per-row reduction is stencil_row_padded's: add.reduceat order over the
-// present slots, bit-exact.  mis[s] = (off[s] mod VN).
+// one window load per +-nx / +-nx^2 neighbour (16-byte when aligned);
+// mis[s] = (off[s] mod VN).  The per-row reduction is branchless: every slot is
+// loaded (absent neighbours read padding / the sentinel value) and add.reduceat's
+// order p0 + (((p1 + p2) + p3) ...) over the present slots is applied with
+// selects: bit-exact.
 template <typename T, int S>
 __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
                                               long long r0, const long long (&off)[S],
@@ -435,11 +391,7 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
 template <typename T, typename E>
 __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
                                                  E& epi, EpiShared<T>& es) {
-  const long long n = S.n;
-  const bool scaled = S.xdiv != nullptr;
-  const T hdiv = scaled ? __ldg(S.xdiv) : T(1);
-  const size_t ld = (size_t)S.ldv;
-  if (S.padded && !scaled) {
+  if (S.padded) {
     const long long nx = S.nx, p2 = nx * nx;
     if (S.dims == 3) {
       const long long off[7] = {-p2, -nx, -1, 0, 1, nx, p2};
@@ -448,10 +400,8 @@ __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const 
       const long long off[5] = {-nx, -1, 0, 1, nx};
       stencil_loop_vec<T, 5>(S, x, off, epi, es);
     }
-  } else if (scaled) {
-    stencil_loop(n, epi, es, [&](long long r) { return stencil_row<T, true>(S, x, r, hdiv); });
   } else {
-    stencil_loop(n, epi, es, [&](long long r) { return stencil_row<T, false>(S, x, r); });
+    stencil_loop(S.n, epi, es, [&](long long r) { return stencil_row<T>(S, x, r); });
   }
 }
 

@@ -198,11 +198,6 @@ struct EpiDot1Warp {
   int bad;
   T acc[KV];
   EpiShared<T>* sm;
-  // fused basis scaling (K_S folded in): V[:, j] = x / h for this CTA's rows
-  const T* vsrc;
-  T* vout;
-  const T* hsrc;
-  T hval;
   __device__ bool skip() const { return *(volatile int*)&sv.h->done != 0; }
   __device__ void init(EpiShared<T>& s, unsigned char*) {
     sm = &s;
@@ -210,16 +205,14 @@ struct EpiDot1Warp {
     for (int q = 0; q < KV; ++q) acc[q] = T(0);
     ss = T(0);
     bad = 0;
-    hval = hsrc ? __ldg(hsrc) : T(1);
   }
   __device__ T on_row(long long r, T y) {
-    if (vout) vout[r] = div_rn(vsrc[r], hval);   // krylov.py:148, same IEEE division
     w[r] = y;
     ss = fma_rn(y, y, ss);
     bad |= !isfinite(y);
     return y;
   }
-  // one 16-byte row group (vectorised stencil loop; never with fused scaling)
+  // one 16-byte row group (vectorised stencil loop)
   static constexpr bool kVecRows = true;
   __device__ void on_rows(long long r0, T (&y)[VN], int cnt, T* ysp) {
     if (cnt == VN) {
@@ -603,7 +596,7 @@ static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& e
     if (occ < 1) occ = 1;
   });
   // the padded (branchless) path deals tiles of one 16-byte row group per thread
-  const long long tile_rows = S.padded && !S.xdiv ? (long long)kSpConsumers * Vec<T>::n : kSpTile;
+  const long long tile_rows = S.padded ? (long long)kSpConsumers * Vec<T>::n : kSpTile;
   long long tiles = (S.n + tile_rows - 1) / tile_rows;
   long long G = (long long)num_sms() * occ;
   if (tiles < G) G = tiles;
@@ -630,21 +623,16 @@ cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* no
 }
 
 template <typename T, typename M>
-cudaError_t launch_spmv_dot1(const M& A0, const T* x, T* w, const T* V, long long ldv, int k,
-                             StateView<T> sv, WsView ws, cudaStream_t st, const T* xdiv,
-                             T* vout) {
-  M A = A0;
-  A.xdiv = xdiv;
+cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
+                             StateView<T> sv, WsView ws, cudaStream_t st) {
   auto reg = [&](auto tag) {
     constexpr int KV = decltype(tag)::value;
     EpiDot1Warp<T, KV> e{};
     e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
     e.part = static_cast<T*>(ws.part);
     e.counter = ws.counter;
-    e.vsrc = x; e.vout = xdiv ? vout : nullptr; e.hsrc = xdiv;
     return launch_matrix(A, x, e, 0, st);
   };
-  if (xdiv && k > 8 * kSpConsumerWarps) return cudaErrorInvalidValue;   // fused scaling: k <= 64
   switch ((k + kSpConsumerWarps - 1) / kSpConsumerWarps) {
     case 1: return reg(std::integral_constant<int, 1>{});
     case 2: return reg(std::integral_constant<int, 2>{});
@@ -697,8 +685,7 @@ cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, c
   template cudaError_t launch_residual<T, M>(const M&, const T*, const T*, T*, double*,         \
                                              mpg_state_header*, WsView, cudaStream_t, int);    \
   template cudaError_t launch_spmv_dot1<T, M>(const M&, const T*, T*, const T*, long long, int, \
-                                              StateView<T>, WsView, cudaStream_t, const T*,    \
-                                              T*);                                             \
+                                              StateView<T>, WsView, cudaStream_t);             \
   template cudaError_t launch_poly_op<T, M>(const M&, const mpg_poly_op&, const T*, T*, T*, T*, \
                                             T*, const mpg_state_header*, long long, WsView,    \
                                             cudaStream_t);

@@ -108,8 +108,7 @@ cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* no
                             mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw = 0);
 template <typename T, typename M>
 cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
-                             StateView<T> sv, WsView ws, cudaStream_t st,
-                             const T* xdiv = nullptr, T* vout = nullptr);
+                             StateView<T> sv, WsView ws, cudaStream_t st);
 template <typename T, typename M>
 cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, T* t0, T* t1,
                            T* t2, const mpg_state_header* gate, long long n, WsView ws,

@@ -430,7 +430,7 @@ cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long lo
                              T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st, const T* jdiag,
                              T* zout) {
   const int k = j + 1;
-  if (k > kMegaMaxK || k + 2 > kMegaMaxCols || !SV.padded || SV.xdiv) return cudaErrorInvalidValue;
+  if (k > kMegaMaxK || k + 2 > kMegaMaxCols || !SV.padded) return cudaErrorInvalidValue;
   const int kv = (k + 7) / 8;
 #define MEGA_CASE(KVV)                                                                            \
   case KVV:                                                                                       \
