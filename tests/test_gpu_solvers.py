@@ -304,20 +304,26 @@ def cfg2_reference():
     return load_json("reference_cfg2.json")["runs"]
 
 
-@pytest.mark.parametrize("solver", ["ir", "fp64"])
+@pytest.mark.parametrize("solver", ["ir", "fp64", "fd1000"])
 def test_cfg2_laplace3d150_full_solve_vs_reference(solver, cfg2_reference):
-    """BASELINE configs[1] at full size against the reference's own run
-    (tests/golden/reference_cfg2.json: 2387 fp64 / 2400 IR iterations,
-    ~20 / ~13 CPU-minutes): same count (+-2 %), every restart-boundary
+    """BASELINE configs[1] at full size against the reference's own runs
+    (tests/golden/reference_cfg2.json: 2387 fp64 / 2400 IR / 2316 GMRES-FD
+    switching at 1000 iterations; ~20 / ~13 / ~10 CPU-minutes): same count (+-2 %), every restart-boundary
     residual within 2x, final fp64 residual <= 1e-10, solution within 1e-8
     relative on a 4101-point strided sample."""
     g = cfg2_reference[f"laplace3d:150/{solver}/m50"]
     A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, 150))
     b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
     crit = P.StopCriteria(rtol=1e-10, m=50)
-    rep = P.gmres_ir(A, b, criteria=crit) if solver == "ir" else P.gmres_restarted(A, b, criteria=crit)
+    if solver == "ir":
+        rep = P.gmres_ir(A, b, criteria=crit)
+    elif solver == "fp64":
+        rep = P.gmres_restarted(A, b, criteria=crit)
+    else:
+        rep = P.gmres_fd(A, b, criteria=crit, switch_iter=int(solver[2:]))
     assert rep.converged
-    assert iters_match(rep, g, 50), (rep.total_iters, g["total_iters"])
+    assert iters_match(rep, g, 50, name=f"laplace3d:150/{solver}/m50"), (rep.total_iters, g["total_iters"],
+                                                                         rep.iters_fp32, g["iters_fp32"])
     # residual trajectory: within 2x of the reference at every restart boundary
     # while it is well above the tolerance; in the last cycles the per-cycle
     # reduction swings with the summation order (e.g. cfg3 IR: 6.1e-10 ->
