@@ -454,7 +454,7 @@ def main():
     else:
         out = native_arm(args, rank, world)
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the CPU baseline rides on the N=1 line only
             v, dt = cpu_sample(1)
             out["cpu_baseline"] = {"value": round(v, 3), "unit": "s", "cores": 1, "kind": "port",
                                    "sample": f"oracle solve_ir one 50-iteration IR cycle ({dt:.1f} s), "
