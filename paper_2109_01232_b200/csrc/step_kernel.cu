@@ -45,6 +45,24 @@ constexpr int kColDot1 = 0;
 constexpr int kColDot2 = kMegaMaxCols;
 constexpr int kColNorm = 2 * kMegaMaxCols;
 
+#ifdef MPG_MEGA_TIMING
+// A/B instrumentation (tools/mega_phases.py): per-CTA globaltimer stamps at the
+// phase boundaries of step MPG_MEGA_TIMING
+__device__ unsigned long long g_mega_t[148 * 2][10];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MEGA_STAMP(i) \
+  if (j == MPG_MEGA_TIMING && threadIdx.x == 0 && blockIdx.x < 296) g_mega_t[blockIdx.x][i] = gtimer();
+extern "C" int mpg_debug_mega_times(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_mega_t, sizeof(g_mega_t));
+}
+#else
+#define MEGA_STAMP(i)
+#endif
+
 __device__ __forceinline__ void group_sync(int grp) {
   asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
 }
@@ -63,6 +81,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1)
 k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
             T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout) {
   if (gated(sv.h)) return;
+  MEGA_STAMP(0)
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
   constexpr int RPW = RB / 8;
@@ -123,6 +142,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   __syncthreads();
+  MEGA_STAMP(1)
 
   // --------------------------------------------------------- P1b c1 = V^T w
   {
@@ -182,7 +202,9 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     for (int w = 0; w < kMegaWarps; ++w) b |= badw[w];
     part[(size_t)(kColDot1 + k + 1) * kMaxParts + blockIdx.x] = b ? T(1) : T(0);
   }
+  MEGA_STAMP(2)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B1
+  MEGA_STAMP(3)
   for (int c = warp; c < k + 2; c += kMegaWarps) {
     const T s = sum_column(part, kColDot1 + c, G);
     if (lane == 0) c1v[c] = s;
@@ -264,7 +286,9 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     for (int g = 0; g < kMegaGroups; ++g) t += cred[g][tid];
     part[(size_t)(kColDot2 + tid) * kMaxParts + blockIdx.x] = t;
   }
+  MEGA_STAMP(4)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B2
+  MEGA_STAMP(5)
   for (int c = warp; c < k; c += kMegaWarps) {
     const T s = sum_column(part, kColDot2 + c, G);
     if (lane == 0) c2v[c] = s;
@@ -326,7 +350,9 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     for (int w = 0; w < kMegaWarps; ++w) t += red[w];
     part[(size_t)kColNorm * kMaxParts + blockIdx.x] = t;
   }
+  MEGA_STAMP(6)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B3
+  MEGA_STAMP(7)
   if (warp == 0) {
     const T s = sum_column(part, kColNorm, G);
     if (lane == 0) red[0] = s;
@@ -364,6 +390,8 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
       }
     }
   }
+  __syncthreads();
+  MEGA_STAMP(8)
 }
 
 // ------------------------------------------------------------------ launch
