@@ -323,6 +323,11 @@ __device__ __forceinline__ T row_reduce(const Get& get, int len) {
 // visible; a no-op for a normal launch), and lets its own successor launch
 // early with pdl_trigger().  Every kernel launched with launch_k(pdl = true)
 // calls pdl_wait() before it reads anything a predecessor wrote.
+// Bulk (TMA-engine) prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -44,6 +44,10 @@ constexpr int kMegaMaxCols = 72;              // k + 2 <= kMegaMaxCols (m <= 64)
 constexpr int kColDot1 = 0;
 constexpr int kColDot2 = kMegaMaxCols;
 constexpr int kColNorm = 2 * kMegaMaxCols;
+// L2 bulk prefetch of basis blocks ahead of the barrier-paced phases (A/B: -DMPG_MEGA_PF=0)
+#ifndef MPG_MEGA_PF
+#define MPG_MEGA_PF 1
+#endif
 
 #ifdef MPG_MEGA_TIMING
 // A/B instrumentation (tools/mega_phases.py): per-CTA globaltimer stamps at the
@@ -202,6 +206,12 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     for (int w = 0; w < kMegaWarps; ++w) b |= badw[w];
     part[(size_t)(kColDot1 + k + 1) * kMaxParts + blockIdx.x] = b ? T(1) : T(0);
   }
+  // the basis blocks P2 starts with do not depend on c1: stage them into L2
+  // while the grid waits at B1
+  if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k && grp < nb) {
+    const long long b0 = bstart(grp);
+    if (b0 + RB <= n) prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + b0, RB * sizeof(T));
+  }
   MEGA_STAMP(2)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B1
   MEGA_STAMP(3)
@@ -233,6 +243,12 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
       const long long b0 = bstart(t);
       const long long r = b0 + (long long)lane * VN;
       const bool in = r < n;
+      // the barriers below keep the group's warps in lock step, so the basis
+      // loads of the next block are staged into L2 ahead of time
+      if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k && t + kMegaGroups < nb) {
+        const long long bn = bstart(t + kMegaGroups);
+        if (bn + RB <= n) prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + bn, RB * sizeof(T));
+      }
       T v[KV][VN], u[VN];
 #pragma unroll
       for (int q = 0; q < KV; ++q) {
@@ -285,6 +301,10 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
 #pragma unroll
     for (int g = 0; g < kMegaGroups; ++g) t += cred[g][tid];
     part[(size_t)(kColDot2 + tid) * kMaxParts + blockIdx.x] = t;
+  }
+  if (MPG_MEGA_PF && lane < k && warp < nb) {   // P3's first block per warp, likewise
+    const long long b0 = bstart(warp);
+    if (b0 + RB <= n) prefetch_l2_bulk(V + (size_t)lane * ldv + b0, RB * sizeof(T));
   }
   MEGA_STAMP(4)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B2
