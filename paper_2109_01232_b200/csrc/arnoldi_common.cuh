@@ -101,10 +101,17 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// A/B: -DMPG_BAR_SC=1 restores the sequentially consistent fences
+// (__threadfence) around the arrival; the default uses acquire/release
+// ordering: arrival atom.acq_rel, release red.release, poll ld.acquire.
+#ifndef MPG_BAR_SC
+#define MPG_BAR_SC 0
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned g0 = ld_acquire_u32(gen);
+#if MPG_BAR_SC
     __threadfence();
     if (atomicAdd(count, 1u) == gridDim.x - 1) {
       atomicExch(count, 0u);
@@ -114,6 +121,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
       while (ld_acquire_u32(gen) == g0) __nanosleep(20);
     }
     __threadfence();
+#else
+    unsigned old;
+    // release: this CTA's writes (ordered before by bar.sync) precede the
+    // arrival; acquire: the last arriver sees every CTA's writes
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(count) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(count) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gen) : "memory");
+    } else {
+      while (ld_acquire_u32(gen) == g0) __nanosleep(20);
+    }
+#endif
   }
   __syncthreads();
 }

@@ -67,6 +67,18 @@ extern "C" int mpg_debug_mega_times(unsigned long long* out) {
 #define MEGA_STAMP(i)
 #endif
 
+// P2 blocks per barrier pair: 2 while the doubled basis registers fit the
+// 64-register budget of 1024-thread CTAs (fp32 KV <= 4, fp64 KV <= 3: no or
+// few-byte spills).  Measured at cfg2 IR: P2 64.5 -> 62.3 us at k = 27, solve
+// 0.500 -> 0.4925 s; bitwise identical iterates.  A/B: -DMPG_MEGA_U2_KV=0.
+#ifndef MPG_MEGA_U2_KV
+#define MPG_MEGA_U2_KV 4
+#endif
+template <typename T, int KV>
+struct MegaU {
+  static constexpr int u = KV <= (sizeof(T) == 8 ? (MPG_MEGA_U2_KV < 3 ? MPG_MEGA_U2_KV : 3) : MPG_MEGA_U2_KV) ? 2 : 1;
+};
+
 __device__ __forceinline__ void group_sync(int grp) {
   asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
 }
@@ -97,8 +109,9 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   const int nb = (long long)blockIdx.x < nblk ? (int)((nblk - 1 - blockIdx.x) / G + 1) : 0;
   extern __shared__ __align__(16) unsigned char smraw[];
   T* wsm = reinterpret_cast<T*>(smraw);
-  __shared__ __align__(16) T upart[kMegaGroups][8][RB];
-  __shared__ __align__(16) T xs[kMegaGroups][RB];
+  constexpr int U = MegaU<T, KV>::u;
+  __shared__ __align__(16) T upart[kMegaGroups][8][U * RB];
+  __shared__ __align__(16) T xs[kMegaGroups][U * RB];
   __shared__ T cred[kMegaGroups][kMegaMaxCols];
   __shared__ T c1v[kMegaMaxCols];
   __shared__ T c2v[kMegaMaxCols];
@@ -234,59 +247,81 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   }
 
   // ------------------------------------ P2 w' = w - V c1 ; c2 = V^T w'
+  // U blocks of the group per barrier pair (blocks t and t + 4 when U = 2:
+  // twice the loads in flight between barriers; the per-row sums and the
+  // accumulation order over blocks are unchanged, so results are bitwise the
+  // same as with U = 1)
   {
     T acc[KV];
 #pragma unroll
     for (int q = 0; q < KV; ++q) acc[q] = T(0);
-    const int rrow = gw * RPW + lane;
-    for (int t = grp; t < nb; t += kMegaGroups) {
-      const long long b0 = bstart(t);
-      const long long r = b0 + (long long)lane * VN;
-      const bool in = r < n;
+    constexpr int RL = (U * RPW <= 32) ? U * RPW : 32;   // reducing lanes
+    const int ub_r = lane / RPW, rrow = gw * RPW + lane % RPW;
+    for (int t = grp; t < nb; t += kMegaGroups * U) {
       // the barriers below keep the group's warps in lock step, so the basis
-      // loads of the next block are staged into L2 ahead of time
-      if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k && t + kMegaGroups < nb) {
-        const long long bn = bstart(t + kMegaGroups);
-        if (bn + RB <= n) prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + bn, RB * sizeof(T));
+      // loads of the next block(s) are staged into L2 ahead of time
+      if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k) {
+#pragma unroll
+        for (int ub = 0; ub < U; ++ub) {
+          const long long bn = bstart(t + (U + ub) * kMegaGroups);
+          if (t + (U + ub) * kMegaGroups < nb && bn + RB <= n)
+            prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + bn, RB * sizeof(T));
+        }
       }
-      T v[KV][VN], u[VN];
+      T v[U][KV][VN], u[U][VN];
 #pragma unroll
-      for (int q = 0; q < KV; ++q) {
-        const int i = gw + 8 * q;
-        if (in && i < k) vload_cs(V + (size_t)i * ldv + r, v[q]);
-        else {
+      for (int ub = 0; ub < U; ++ub) {
+        const long long r = bstart(t + ub * kMegaGroups) + (long long)lane * VN;
+        const bool in = t + ub * kMegaGroups < nb && r < n;
 #pragma unroll
-          for (int e = 0; e < VN; ++e) v[q][e] = T(0);
+        for (int q = 0; q < KV; ++q) {
+          const int i = gw + 8 * q;
+          if (in && i < k) vload_cs(V + (size_t)i * ldv + r, v[ub][q]);
+          else {
+#pragma unroll
+            for (int e = 0; e < VN; ++e) v[ub][q][e] = T(0);
+          }
         }
       }
 #pragma unroll
-      for (int e = 0; e < VN; ++e) u[e] = T(0);
+      for (int ub = 0; ub < U; ++ub) {
 #pragma unroll
-      for (int q = 0; q < KV; ++q) {
-        const int i = gw + 8 * q;
-        const T c = i < k ? c1v[i] : T(0);
+        for (int e = 0; e < VN; ++e) u[ub][e] = T(0);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) u[e] = fma_rn(v[q][e], c, u[e]);
+        for (int q = 0; q < KV; ++q) {
+          const int i = gw + 8 * q;
+          const T c = i < k ? c1v[i] : T(0);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) u[ub][e] = fma_rn(v[ub][q][e], c, u[ub][e]);
+        }
+        vstore(upart[grp][gw] + ub * RB + lane * VN, u[ub]);
       }
-      vstore(upart[grp][gw] + lane * VN, u);
       group_sync(grp);
-      if (lane < RPW) {
+      if (lane < RL) {
+        const int tb = t + ub_r * kMegaGroups;
+        const long long b0 = bstart(tb);
         T s = T(0);
 #pragma unroll
-        for (int ww = 0; ww < 8; ++ww) s += upart[grp][ww][rrow];
-        T* wr = wptr(t) + rrow;
-        const bool rin = b0 + rrow < n;
-        const T xr = rin ? sub_rn(*wr, s) : T(0);
-        if (CACHE || rin) *wr = xr;
-        xs[grp][rrow] = xr;
+        for (int ww = 0; ww < 8; ++ww) s += upart[grp][ww][ub_r * RB + rrow];
+        const bool rin = tb < nb && b0 + rrow < n;
+        T xr = T(0);
+        if (tb < nb) {
+          T* wr = wptr(tb) + rrow;
+          if (rin) xr = sub_rn(*wr, s);
+          if (CACHE || rin) *wr = xr;
+        }
+        xs[grp][ub_r * RB + rrow] = xr;
       }
       group_sync(grp);
-      T xv[VN];
-      vload_smem(xs[grp] + lane * VN, xv);
 #pragma unroll
-      for (int q = 0; q < KV; ++q)
+      for (int ub = 0; ub < U; ++ub) {
+        T xv[VN];
+        vload_smem(xs[grp] + ub * RB + lane * VN, xv);
 #pragma unroll
-        for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[q][e], xv[e], acc[q]);
+        for (int q = 0; q < KV; ++q)
+#pragma unroll
+          for (int e = 0; e < VN; ++e) acc[q] = fma_rn(v[ub][q][e], xv[e], acc[q]);
+      }
     }
 #pragma unroll
     for (int q = 0; q < KV; ++q) {
@@ -443,7 +478,7 @@ static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, lon
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         optin - (int)sizeof(T) * (kMegaGroups * 9 * 32 * Vec<T>::n + 3 * kMegaMaxCols * 2) - 2048);
+                         optin - (int)sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * 32 * Vec<T>::n + 3 * kMegaMaxCols * 2) - 2048);
     cudaGetLastError();
   });
   count_launch();
@@ -466,7 +501,7 @@ static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, lo
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   // static shared memory of the kernel (upart, xs, column scratch) + headroom
-  const size_t stat = sizeof(T) * (kMegaGroups * 9 * RB + 3 * kMegaMaxCols * 2) + 2048;
+  const size_t stat = sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * RB + 3 * kMegaMaxCols * 2) + 2048;
   if (cache + stat <= (size_t)optin)
     return launch_mega_k<T, S, KV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache, jdiag,
                                          zout);
