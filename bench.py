@@ -102,7 +102,9 @@ class ClockSampler:
 def cycle_bytes(n: int, nnz: int, m: int, s: int, storage: str = "csr") -> dict[str, float]:
     """Algorithmic bytes per cycle for each fused kernel class, s = value size.
     CSR: values + col_idx + row_ptr; stencil: the present values only."""
-    if storage == "stencil":
+    if storage == "stencil-const":
+        spmv = 2 * n * s                                      # coefficients in registers: x once + y once
+    elif storage == "stencil":
         spmv = nnz * s + 2 * n * s                            # values + x once + y once
     else:
         spmv = nnz * (s + 4) + 4 * (n + 1) + 2 * n * s       # CSR + x once + y once
@@ -122,7 +124,8 @@ def split_cycle_bytes(model: dict, n: int, nnz: int, m: int, s: int, storage: st
     """K_A split into two launches (the default): the SpMV class moves the
     matrix, x once and w once; the pass-1 dot kernel reads V[0..k) and w.
     Kernel-level algorithmic bytes: each launch's inputs and outputs once."""
-    spmv = (nnz * s if storage == "stencil" else nnz * (s + 4) + 4 * (n + 1)) + 2 * n * s
+    mat = {"stencil-const": 0, "stencil": nnz * s}.get(storage, nnz * (s + 4) + 4 * (n + 1))
+    spmv = mat + 2 * n * s
     out = dict(model)
     out["spmv_dot1"] = m * spmv
     out["dot1"] = sum((k + 1) * n * s for k in range(1, m + 1))

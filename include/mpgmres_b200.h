@@ -127,8 +127,11 @@ int mpg_generate_stencil(int kind, int64_t nx, double convection, double stretch
 /* Stencil-specialised SpMV storage (the north star's stencil path).  Checks
  * that the CSR pattern is exactly the Dirichlet 5-point (dims 2, n = nx^2) or
  * 7-point (dims 3, n = nx^3) stencil in canonical order and packs the values
- * slot-major into dia[S][ldv] (S = 5 or 7; absent neighbours stored as 0 and
- * never read).  *bad (device int32, caller zeroes it) != 0 on mismatch. */
+ * slot-major into dia[S][ldv] (S = 5 or 7; absent neighbours hold a NaN
+ * sentinel payload).  dia must hold S*ldv + 64 elements: the tail receives a
+ * header (dia[S*ldv] = 1 when every slot has a single coefficient, then the S
+ * coefficients) that lets the solver's SpMV stream x alone, bit-identically.
+ * *bad (device int32, caller zeroes it) != 0 on mismatch. */
 int mpg_stencil_pack(int prec, int dims, int64_t nx, int64_t n, const int32_t* row_ptr,
                      const int32_t* col_idx, const void* values, void* dia, int64_t ldv,
                      int32_t* bad, void* stream);

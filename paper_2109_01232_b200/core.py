@@ -145,6 +145,13 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+# elements after the S x ldv packed stencil values: the constant-coefficient
+# header written by mpg_stencil_pack* (csrc/spmv.cuh kDiaTail) and its scratch
+DIA_TAIL = 64
+# A/B switch: False keeps the constant-coefficient SpMV path off for new packs
+STENCIL_CONST = True
+
+
 def padded_length(n: int) -> int:
     """Vectors the library owns are padded to a multiple of 64 elements."""
     return max(64, (n + 63) // 64 * 64)
@@ -341,14 +348,26 @@ class CsrMatrix:
     def _pack(self, dims: int, nx: int) -> torch.Tensor | None:
         S = 7 if dims == 3 else 5
         ldv = padded_length(self.n_rows)
-        dia = torch.zeros(S * ldv, dtype=self.values.dtype, device=self.values.device)
+        # S x ldv packed values + the constant-coefficient header / scratch tail
+        dia = torch.zeros(S * ldv + DIA_TAIL, dtype=self.values.dtype, device=self.values.device)
         bad = torch.zeros(1, dtype=torch.int32, device=self.values.device)
         _lib.call("mpg_stencil_pack", self.precision.code, dims, nx, self.n_rows, ptr(self.row_ptr),
                   ptr(self.col_idx), ptr(self.values), ptr(dia), ldv, ptr(bad), stream_handle())
         if int(bad.item()) != 0:
             return None
+        if not STENCIL_CONST:
+            dia[S * ldv] = 0          # keep the coefficient-stream path off (A/B, tests)
         self._dia = dia
         return dia
+
+    def stencil_const(self) -> bool:
+        """True when the packed stencil has one coefficient per slot (the SpMV
+        then streams x alone; csrc/spmv.cuh StencilConst)."""
+        d = self.dia()
+        if d is None:
+            return False
+        S = 7 if self.stencil_shape()[0] == 3 else 5
+        return bool(d[S * padded_length(self.n_rows)].item() != 0)
 
     def dia(self) -> torch.Tensor | None:
         """Slot-major packed values (S x ldv) for the stencil path, or None."""

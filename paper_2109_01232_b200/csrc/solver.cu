@@ -90,6 +90,7 @@ static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, con
                       d.stencil_dims, d.row0};
     const long long plane = d.stencil_dims == 3 ? (long long)d.stencil_nx * d.stencil_nx : d.stencil_nx;
     S.padded = d.halo >= plane ? 1 : 0;
+    S.konst = 1;   // descriptor dia buffers are packed by mpg_stencil_pack* (header in the tail)
     return f(S);
   }
   return f(CsrView<TP>{d.row_ptr, d.col_idx, csr_vals, d.n});
@@ -255,6 +256,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
                        d.stencil_dims, d.row0};
       S.padded = 1;
+      S.konst = 1;
       // the last persistent step hands the four-launch steps V[:, j+1]; they apply M themselves
       const bool next_mega = j + 2 <= kMegaMaxK && j + 1 < m_limit;
       TRY(launch_step_mega<T>(S, jac1 ? zbuf : xin, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st,

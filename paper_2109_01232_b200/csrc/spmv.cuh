@@ -164,6 +164,9 @@ struct StencilView {
   // 1: every SpMV input has >= one grid plane of readable padding (or halo)
   // on both sides, so rows use the branchless sentinel path below
   int padded = 0;
+  // 1: vals carries the constant-coefficient header (buffers packed by
+  // launch_stencil_pack with the kDiaTail tail); padded path only
+  int konst = 0;
 };
 
 // Absent stencil slots (neighbour outside the grid) hold this NaN payload in
@@ -191,12 +194,14 @@ template <> __host__ __device__ inline double absent_value<double>() {
 #endif
 }
 
-// exact q = r / nx for r < 2^32, nx < 2^16: ((uint64)r * ceil(2^48/nx)) >> 48
+// exact q = r / nx for r < 2^32, 2 <= nx < 2^32: q = hi64(r * M) with
+// M = floor((2^64 - 1) / nx) + 1 (M - 2^64/nx lies in (0, 1], so the error term
+// r * (M - 2^64/nx) / 2^64 < 1/nx cannot carry into the quotient)
 __device__ __forceinline__ unsigned div_nx(unsigned r, unsigned long long magic) {
-  return (unsigned)(((unsigned long long)r * magic) >> 48);
+  return (unsigned)__umul64hi((unsigned long long)r, magic);
 }
 __host__ __device__ inline unsigned long long nx_magic(unsigned nx) {
-  return ((1ULL << 48) + nx - 1) / nx;
+  return ~0ull / nx + 1ull;
 }
 
 template <typename T, int S>
@@ -249,6 +254,33 @@ __device__ __forceinline__ T stencil_row(const StencilView<T>& S, const T* __res
     px[s] = pr[s] ? __ldg(x + r + off[s]) : T(0);
   }
   return stencil_reduce<T, 5>(pr, pv, px);
+}
+
+// Constant-coefficient stencils.  Every packed dia buffer is S * ldv values
+// followed by a kDiaTail-element tail whose header, written by the packing
+// launch (launch_stencil_pack), reads h[0] = 1 when each slot holds one and the
+// same value (bit pattern) in every row where it is present -- Laplace and
+// uniform-convection stencils -- and h[1 + s] = that value.  The SpMV then
+// takes the coefficients from registers and derives presence from the grid
+// coordinates, so it streams x alone; the products and their summation order
+// are unchanged (bit-identical results).  The values stay stored for the
+// scalar / CSR paths.  Bytes 64.. of the tail are the packing scratch.
+constexpr int kDiaTail = 64;
+template <typename T, int S>
+struct StencilConst {
+  bool on;
+  T kc[S];
+  unsigned long long mg;   // nx_magic(nx)
+};
+template <typename T, int S>
+__device__ __forceinline__ StencilConst<T, S> stencil_const(const StencilView<T>& SV) {
+  StencilConst<T, S> c;
+  const T* h = SV.vals + (size_t)S * SV.ldv;
+  c.on = SV.konst && __ldg(h) != T(0);
+#pragma unroll
+  for (int s = 0; s < S; ++s) c.kc[s] = c.on ? __ldg(h + 1 + s) : T(0);
+  c.mg = nx_magic((unsigned)SV.nx);
+  return c;
 }
 
 // Tiles are dealt round-robin (tile = blockIdx.x + i * gridDim.x): the whole grid
@@ -314,13 +346,35 @@ __device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)
 template <typename T, int S>
 __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
                                               long long r0, const long long (&off)[S],
-                                              const int (&mis)[S], T (&y)[Vec<T>::n]) {
+                                              const int (&mis)[S], const StencilConst<T, S>& K,
+                                              T (&y)[Vec<T>::n]) {
   constexpr int VN = Vec<T>::n;
   constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
   const size_t ld = (size_t)SV.ldv;
   T pv[S][VN], px[S][VN];
+  if (K.on) {   // coefficients from registers, presence from the grid coordinates
+    const unsigned nx = (unsigned)SV.nx;
 #pragma unroll
-  for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
+    for (int e = 0; e < VN; ++e) {
+      const unsigned ur = (unsigned)(r0 + SV.row0) + (unsigned)e;
+      const unsigned q = div_nx(ur, K.mg);
+      const unsigned ix = ur - q * nx;
+      bool pr[S];
+      if constexpr (S == 7) {
+        const unsigned iz = div_nx(q, K.mg);
+        const unsigned iy = q - iz * nx;
+        pr[0] = iz > 0; pr[1] = iy > 0; pr[2] = ix > 0; pr[3] = true;
+        pr[4] = ix + 1 < nx; pr[5] = iy + 1 < nx; pr[6] = iz + 1 < nx;
+      } else {
+        pr[0] = q > 0; pr[1] = ix > 0; pr[2] = true; pr[3] = ix + 1 < nx; pr[4] = q + 1 < nx;
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) pv[s][e] = pr[s] ? K.kc[s] : absent_value<T>();
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
+  }
   vload(x + r0, px[C]);
   const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
 #pragma unroll
@@ -367,6 +421,7 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
   const long long n = SV.n;
   int mis[S];
   stencil_mis<T, S>(off, mis);
+  const StencilConst<T, S> K = stencil_const<T, S>(SV);
   const long long ntiles = (n + TILE - 1) / TILE;
   int t = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
@@ -377,7 +432,7 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
     if (rr < nrows) {
       const long long r0 = a + rr;
       T y[VN];
-      stencil_group<T, S>(SV, x, r0, off, mis, y);
+      stencil_group<T, S>(SV, x, r0, off, mis, K, y);
       epi_rows(epi, r0, y, min(VN, nrows - rr), ys + rr);
     }
     if constexpr (needs_tiles<E>::value) {

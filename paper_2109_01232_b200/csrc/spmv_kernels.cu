@@ -668,6 +668,70 @@ cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, 
   return launch_matrix(A, e.src, e, 0, st);
 }
 
+// Constant-coefficient scan of packed values: per slot, the min and max bit
+// pattern over the present entries (u64 atomics into the tail scratch).
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_stencil_const_scan(int S, const T* __restrict__ dia, long long ldv,
+                                                                 long long n, unsigned long long* mm) {
+  unsigned long long lo[7], hi[7];
+#pragma unroll
+  for (int s = 0; s < 7; ++s) { lo[s] = ~0ull; hi[s] = 0ull; }
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+       r += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+      if (s < S) {
+        const T v = dia[(size_t)s * ldv + r];
+        if (present(v)) {
+          unsigned long long b;
+          if constexpr (sizeof(T) == 8) b = (unsigned long long)__double_as_longlong(v);
+          else b = (unsigned long long)__float_as_uint(v);
+          lo[s] = b < lo[s] ? b : lo[s];
+          hi[s] = b > hi[s] ? b : hi[s];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < 7; ++s) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long l2 = __shfl_xor_sync(0xffffffffu, lo[s], o);
+      const unsigned long long h2 = __shfl_xor_sync(0xffffffffu, hi[s], o);
+      lo[s] = l2 < lo[s] ? l2 : lo[s];
+      hi[s] = h2 > hi[s] ? h2 : hi[s];
+    }
+    if ((threadIdx.x & 31) == 0 && s < S) {
+      atomicMin(mm + s, lo[s]);
+      atomicMax(mm + 7 + s, hi[s]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_stencil_const_header(int S, T* h, const unsigned long long* mm, int enable) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  bool on = enable != 0;
+  for (int s = 0; s < S; ++s) on = on && (mm[s] == mm[7 + s] || mm[s] == ~0ull);   // one value, or never present
+  h[0] = on ? T(1) : T(0);
+  for (int s = 0; s < S; ++s) {
+    const unsigned long long b = mm[s] == ~0ull ? 0ull : mm[s];
+    T v;
+    if constexpr (sizeof(T) == 8) v = __longlong_as_double((long long)b);
+    else v = __uint_as_float((unsigned)b);
+    h[1 + s] = on ? v : T(0);
+  }
+}
+
+// MPG_STENCIL_CONST=0 keeps the header off (A/B of the coefficient-stream path)
+static int stencil_const_env() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("MPG_STENCIL_CONST");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v;
+}
+
 template <typename T>
 cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, const int32_t* rp,
                                 const int32_t* ci, const T* v, T* out, long long ldv, int* bad,
@@ -677,6 +741,17 @@ cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, c
   if (G < 1) G = 1;
   count_launch();
   k_stencil_pack<T><<<(unsigned)G, kThreads, 0, st>>>(dims, nx, row0, n, rp, ci, v, out, ldv, bad);
+  // constant-coefficient header in the tail (the caller allocates S*ldv + kDiaTail)
+  const int S = dims == 3 ? 7 : 5;
+  T* h = out + (size_t)S * ldv;
+  unsigned long long* mm = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(h) + 64);
+  cudaError_t e = cudaMemsetAsync(mm, 0xff, 7 * sizeof(unsigned long long), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(mm + 7, 0, 7 * sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  k_stencil_const_scan<T><<<(unsigned)G, kThreads, 0, st>>>(S, out, ldv, n, mm);
+  count_launch();
+  k_stencil_const_header<T><<<1, 32, 0, st>>>(S, h, mm, stencil_const_env());
   return cudaGetLastError();
 }
 

@@ -137,6 +137,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   }
   int mis[S];
   stencil_mis<T, S>(off, mis);
+  const StencilConst<T, S> K = stencil_const<T, S>(SV);
   T ss = T(0);
   int bad = 0;
   for (int L = tid; L < nb * 32; L += kMegaThreads) {
@@ -144,7 +145,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     const long long r0 = bstart(t) + (long long)l * VN;
     T y[VN];
     if (r0 < n) {
-      stencil_group<T, S>(SV, x, r0, off, mis, y);
+      stencil_group<T, S>(SV, x, r0, off, mis, K, y);
 #pragma unroll
       for (int e = 0; e < VN; ++e) y[e] = r0 + e < n ? y[e] : T(0);
     } else {

@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib, timing
-from .core import FP32, FP64, Precision, PrecisionError, device, padded_length, ptr, stream_handle
+from .core import DIA_TAIL, FP32, FP64, Precision, PrecisionError, device, padded_length, ptr, stream_handle
 from .solvers import (LOSS_OF_ACCURACY_FACTOR, STALL_IMPROVEMENT, STALL_RESTARTS, HistoryEntry,
                       SolveReport, StopCriteria, _raise_flags, _relative)
 
@@ -203,7 +203,7 @@ class DistributedStencilSolver:
         for p in {FP64, self.prec}:
             vals = v64 if p is FP64 else v64.to(torch.float32)
             # slot stride = the descriptor's ldv (the kernels index both with it)
-            dia = torch.zeros(S * ld, dtype=p.torch_dtype, device=dev)
+            dia = torch.zeros(S * ld + DIA_TAIL, dtype=p.torch_dtype, device=dev)   # + header tail
             bad = torch.zeros(1, dtype=torch.int32, device=dev)
             _lib.call("mpg_stencil_pack_rows", p.code, part.dims, part.nx, part.row0, n, ptr(rp),
                       ptr(ci), ptr(vals), ptr(dia), ld, ptr(bad), stream_handle())

@@ -304,7 +304,8 @@ class NativeSolve:
                 d.pc_dia = ptr(pc_dia) if pc_dia is not None else None
                 d.halo = self.guard
                 self._keep += [t for t in (dia, dia64, pc_dia) if t is not None]
-                self.storage = "stencil"
+                # one coefficient per slot: the SpMV streams x alone (csrc/spmv.cuh StencilConst)
+                self.storage = "stencil-const" if A.stencil_const() else "stencil"
         self.desc = d
         h = C.c_void_p()
         _lib.call("mpg_solver_create", C.byref(d), C.byref(h))

@@ -489,3 +489,30 @@ def test_cfg5_laplace3d400_assembly_and_first_ir_cycle_vs_reference():
     ref_err = np.linalg.norm(xir - x64) / np.linalg.norm(x64)
     assert ours_err <= 1e-4, ours_err
     assert ref_err > 10 * ours_err, (ref_err, ours_err)
+
+
+@pytest.mark.parametrize("kind,nx,kw,const", [("laplace3d", 33, {}, True), ("laplace2d", 61, {}, True),
+                                              ("convdiff2d", 101, {"convection": 1501.0}, True),
+                                              ("recirc2d", 49, {"convection": 0.5}, False)])
+def test_constant_coefficient_stencil_path_is_bitwise_the_packed_path(kind, nx, kw, const):
+    """Stencils with one coefficient per slot (Laplace, uniform convection) take
+    the coefficient-stream SpMV (csrc/spmv.cuh StencilConst: x only, presence
+    from grid coordinates); the iterate and history equal the packed-values
+    path bit for bit.  Position-dependent stencils (Recirc2D) keep the values."""
+    spec = P.StencilSpec(P.StencilKind(kind), nx, **kw)
+    reps, flags = [], []
+    for on in (True, False):
+        prev, P.core.STENCIL_CONST = P.core.STENCIL_CONST, on
+        try:
+            A = P.generate(spec)
+            b = np.ones(A.n_rows)
+            flags.append(P.convert_matrix(A, P.FP32).stencil_const())
+            reps.append(P.gmres_ir(A, b, criteria=P.StopCriteria(rtol=1e-10, m=30, max_iters=600)))
+        finally:
+            P.core.STENCIL_CONST = prev
+    assert flags == [const, False]
+    a, b_ = reps
+    assert a.total_iters == b_.total_iters
+    assert np.array_equal(a.x, b_.x)
+    assert [(e.iteration, e.implicit, e.explicit) for e in a.residual_history] == \
+           [(e.iteration, e.implicit, e.explicit) for e in b_.residual_history]
