@@ -15,6 +15,9 @@ struct mpg_solver {
   std::map<int, cudaGraphExec_t> graphs;  // per m_limit
   std::map<int, int> graph_launches;      // kernels per graph (for the launch counter)
   cudaStream_t cap = nullptr;
+  // the working-precision dia carries one coefficient per slot (read once at
+  // create from the packing header): the step kernel's KONST instantiation
+  int dia_const = 0;
 };
 
 namespace mpg {
@@ -256,7 +259,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
                        d.stencil_dims, d.row0};
       S.padded = 1;
-      S.konst = 1;
+      S.konst = s->dia_const ? 2 : 0;   // 2: header known on, step kernel KONST instantiation
       // the last persistent step hands the four-launch steps V[:, j+1]; they apply M themselves
       const bool next_mega = j + 2 <= kMegaMaxK && j + 1 < m_limit;
       TRY(launch_step_mega<T>(S, jac1 ? zbuf : xin, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st,
@@ -424,6 +427,17 @@ extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) 
   if (d.dist && (!d.stencil_dims || d.pc_kind != MPG_PC_NONE)) return MPG_EUNSUPPORTED;
   mpg_solver* s = new mpg_solver();
   s->d = d;
+  if (d.stencil_dims && d.dia && !d.dist) {   // constant-coefficient header (spmv.cuh StencilConst)
+    const int S = d.stencil_dims == 3 ? 7 : 5;
+    const size_t es = d.prec == MPG_FP64 ? 8 : 4;
+    const char* hp = static_cast<const char*>(d.dia) + (size_t)S * (d.dia_ld ? d.dia_ld : d.ldv) * es;
+    double h64 = 0.0;
+    float h32 = 0.f;
+    cudaDeviceSynchronize();
+    if (cudaMemcpy(es == 8 ? (void*)&h64 : (void*)&h32, hp, es, cudaMemcpyDeviceToHost) == cudaSuccess)
+      s->dia_const = (es == 8 ? h64 != 0.0 : h32 != 0.f) ? 1 : 0;
+    cudaGetLastError();
+  }
   if (d.pc_kind == MPG_PC_POLY) s->ops.assign(d.pc_ops, d.pc_ops + d.pc_nops);
   s->d.pc_ops = nullptr;
   if (cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking) != cudaSuccess) {

@@ -352,26 +352,7 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
   constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
   const size_t ld = (size_t)SV.ldv;
   T pv[S][VN], px[S][VN];
-  if (K.on) {   // coefficients from registers, presence from the grid coordinates
-    const unsigned nx = (unsigned)SV.nx;
-#pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      const unsigned ur = (unsigned)(r0 + SV.row0) + (unsigned)e;
-      const unsigned q = div_nx(ur, K.mg);
-      const unsigned ix = ur - q * nx;
-      bool pr[S];
-      if constexpr (S == 7) {
-        const unsigned iz = div_nx(q, K.mg);
-        const unsigned iy = q - iz * nx;
-        pr[0] = iz > 0; pr[1] = iy > 0; pr[2] = ix > 0; pr[3] = true;
-        pr[4] = ix + 1 < nx; pr[5] = iy + 1 < nx; pr[6] = iz + 1 < nx;
-      } else {
-        pr[0] = q > 0; pr[1] = ix > 0; pr[2] = true; pr[3] = ix + 1 < nx; pr[4] = q + 1 < nx;
-      }
-#pragma unroll
-      for (int s = 0; s < S; ++s) pv[s][e] = pr[s] ? K.kc[s] : absent_value<T>();
-    }
-  } else {
+  if (!K.on) {
 #pragma unroll
     for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
   }
@@ -386,6 +367,58 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
 #pragma unroll
   for (int e = 0; e < VN - 1; ++e) px[C + 1][e] = px[C][e + 1];
   px[C + 1][VN - 1] = xp;
+  if (K.on) {   // coefficients from registers, presence from the grid coordinates
+    const unsigned nx = (unsigned)SV.nx;
+    const unsigned ur0 = (unsigned)(r0 + SV.row0);
+    const unsigned q0 = div_nx(ur0, K.mg);
+    const unsigned ix0 = ur0 - q0 * nx;
+    bool inner;
+    if constexpr (S == 7) {
+      const unsigned iz0 = div_nx(q0, K.mg);
+      const unsigned iy0 = q0 - iz0 * nx;
+      inner = iy0 >= 1 && iy0 + 2 <= nx && iz0 >= 1 && iz0 + 2 <= nx;
+    } else {
+      inner = q0 >= 1 && q0 + 2 <= nx;
+    }
+    inner = inner && ix0 >= 1 && ix0 + VN + 1 <= nx;
+    if (inner) {   // every slot present in all VN rows: p0 + (((p1 + p2) + p3) ...) directly
+#pragma unroll
+      for (int e = 0; e < VN; ++e) {
+        T rest = mul_rn(K.kc[1], px[1][e]);
+#pragma unroll
+        for (int s = 2; s < S; ++s) rest = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
+        y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
+      }
+      return;
+    }
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {   // boundary groups: per-row presence, no value registers
+      const unsigned ur = ur0 + (unsigned)e;
+      const unsigned q = div_nx(ur, K.mg);
+      const unsigned ix = ur - q * nx;
+      bool pr[S];
+      if constexpr (S == 7) {
+        const unsigned iz = div_nx(q, K.mg);
+        const unsigned iy = q - iz * nx;
+        pr[0] = iz > 0; pr[1] = iy > 0; pr[2] = ix > 0; pr[3] = true;
+        pr[4] = ix + 1 < nx; pr[5] = iy + 1 < nx; pr[6] = iz + 1 < nx;
+      } else {
+        pr[0] = q > 0; pr[1] = ix > 0; pr[2] = true; pr[3] = ix + 1 < nx; pr[4] = q + 1 < nx;
+      }
+      bool have = false;
+      T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const T p = mul_rn(K.kc[s], px[s][e]);
+        const T nrest = add_rn(rest, p);
+        rest = (pr[s] && have) ? nrest : rest;
+        p0 = (pr[s] && !have) ? p : p0;
+        have = have || pr[s];
+      }
+      y[e] = add_rn(p0, rest);
+    }
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < VN; ++e) {
     bool have = false;

@@ -92,7 +92,7 @@ __device__ __forceinline__ T sum_column(const T* part, int col, int G) {
   return warp_sum(s);
 }
 
-template <typename T, int S, int KV, bool CACHE>
+template <typename T, int S, int KV, bool CACHE, bool KONST>
 __global__ void __launch_bounds__(kMegaThreads, 1)
 k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
             T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout) {
@@ -137,7 +137,11 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   }
   int mis[S];
   stencil_mis<T, S>(off, mis);
-  const StencilConst<T, S> K = stencil_const<T, S>(SV);
+  // KONST: the host read the constant-coefficient header at create, so only
+  // the coefficient-stream SpMV is compiled in (and only the packed-values one
+  // otherwise): the 64-register budget holds one path, not both
+  StencilConst<T, S> K = stencil_const<T, S>(SV);
+  K.on = KONST;
   T ss = T(0);
   int bad = 0;
   for (int L = tid; L < nb * 32; L += kMegaThreads) {
@@ -469,7 +473,7 @@ int mega_env() {
   return v;
 }
 
-template <typename T, int S, int KV, bool CACHE>
+template <typename T, int S, int KV, bool CACHE, bool KONST>
 static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
                                  unsigned grid, size_t smem, const T* jdiag, T* zout) {
@@ -478,12 +482,12 @@ static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, lon
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE, KONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * 32 * Vec<T>::n + 3 * kMegaMaxCols * 2) - 2048);
     cudaGetLastError();
   });
   count_launch();
-  return launch_k(false, true, k_step_mega<T, S, KV, CACHE>, dim3(grid), dim3(kMegaThreads), smem, st, SV, x,
+  return launch_k(false, true, k_step_mega<T, S, KV, CACHE, KONST>, dim3(grid), dim3(kMegaThreads), smem, st, SV, x,
                   V, ldv, n, j, w, sv, ws, m_limit, jdiag, zout);
 }
 
@@ -503,10 +507,15 @@ static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, lo
   }
   // static shared memory of the kernel (upart, xs, column scratch) + headroom
   const size_t stat = sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * RB + 3 * kMegaMaxCols * 2) + 2048;
-  if (cache + stat <= (size_t)optin)
-    return launch_mega_k<T, S, KV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache, jdiag,
-                                         zout);
-  return launch_mega_k<T, S, KV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0, jdiag, zout);
+  if (cache + stat <= (size_t)optin) {
+    if (SV.konst == 2)
+      return launch_mega_k<T, S, KV, true, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache,
+                                                 jdiag, zout);
+    return launch_mega_k<T, S, KV, true, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache,
+                                                jdiag, zout);
+  }
+  return launch_mega_k<T, S, KV, false, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0, jdiag,
+                                               zout);
 }
 
 template <typename T>
