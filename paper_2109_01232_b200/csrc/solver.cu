@@ -259,7 +259,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
       StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
                        d.stencil_dims, d.row0};
       S.padded = 1;
-      S.konst = s->dia_const ? 2 : 0;   // 2: header known on, step kernel KONST instantiation
+      S.konst = s.dia_const ? 2 : 0;   // 2: header known on, step kernel KONST instantiation
       // the last persistent step hands the four-launch steps V[:, j+1]; they apply M themselves
       const bool next_mega = j + 2 <= kMegaMaxK && j + 1 < m_limit;
       TRY(launch_step_mega<T>(S, jac1 ? zbuf : xin, V, d.ldv, d.n, j, wj, sv, ws, m_limit, st,
