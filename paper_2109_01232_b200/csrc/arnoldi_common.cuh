@@ -93,6 +93,60 @@ __device__ void givens_column(const StateView<T>& sv, int j, double threshold, b
 }
 
 
+// givens_column by one whole warp: the column, cos and sin are staged in shared
+// memory `sm` (>= 3 * j + 2 elements) by all lanes, lane 0 runs the same
+// rotation sequence on the staged values (identical arithmetic and order), and
+// the lanes write the rotated column back.  Replaces j dependent global
+// load/store round trips of the one-thread version with shared-memory ones.
+template <typename T>
+__device__ void givens_column_warp(const StateView<T>& sv, int j, double threshold, bool brk, int m_limit,
+                                   T* sm) {
+  const int lane = threadIdx.x & 31;
+  T* col = sm;            // j + 2
+  T* cc = sm + j + 2;     // j
+  T* ss = cc + j;         // j
+  for (int i = lane; i <= j + 1; i += 32) col[i] = sv.Hc(j, i);
+  for (int i = lane; i < j; i += 32) {
+    cc[i] = sv.cs[i];
+    ss[i] = sv.sn[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int i = 0; i < j; ++i) {
+      const T c = cc[i], s = ss[i];
+      const T a = col[i], b = col[i + 1];
+      const T top = add_rn(mul_rn(c, a), mul_rn(s, b));
+      col[i + 1] = add_rn(mul_rn(-s, a), mul_rn(c, b));
+      col[i] = top;
+    }
+    const T a = col[j], b = col[j + 1];
+    const T r = hypot_ref(a, b);
+    double res;
+    if (r == T(0)) {
+      sv.cs[j] = T(1);
+      sv.sn[j] = T(0);
+      res = (double)fabs(sv.g[j]);
+    } else {
+      const T c = div_rn(a, r), s = div_rn(b, r);
+      sv.cs[j] = c;
+      sv.sn[j] = s;
+      col[j] = add_rn(mul_rn(c, a), mul_rn(s, b));
+      col[j + 1] = T(0);
+      const T gj = sv.g[j], gj1 = sv.g[j + 1];
+      const T top = add_rn(mul_rn(c, gj), mul_rn(s, gj1));
+      sv.g[j + 1] = add_rn(mul_rn(-s, gj), mul_rn(c, gj1));
+      sv.g[j] = top;
+      res = (double)fabs(sv.g[j + 1]);
+    }
+    sv.implicit[j] = res;
+    sv.h->steps = j + 1;
+    sv.h->breakdown = brk ? 1 : 0;
+    if (brk || res <= threshold || j + 1 >= m_limit) sv.h->done = 1;
+  }
+  __syncwarp();
+  for (int i = lane; i <= j + 1; i += 32) sv.Rc(j, i) = col[i];
+}
+
 // Grid barrier for cooperative launches (every CTA co-resident): shared
 // arrival counter + generation word in the workspace; the last arriver resets
 // the counter before releasing, so the slot is reusable.

@@ -420,10 +420,13 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   __syncthreads();
   const T hs = sqrt_rn(red[0]);
   const bool brk = (double)hs <= sv.h->breakdown_tol * w0;   // krylov.py:146
-  if (blockIdx.x == 0 && tid == 0) {
-    sv.Hc(j, j + 1) = hs;
-    sv.h->h_sub = (double)hs;
-    givens_column(sv, j, sv.h->threshold, brk, m_limit);
+  if (blockIdx.x == 0 && warp == 0) {   // the rotation runs in warp 0 while warps 1.. start P4
+    if (lane == 0) {
+      sv.Hc(j, j + 1) = hs;
+      sv.h->h_sub = (double)hs;
+    }
+    __syncwarp();
+    givens_column_warp(sv, j, sv.h->threshold, brk, m_limit, &cred[0][0]);   // cred is free after B2
   }
   if (brk) return;   // no new basis vector on breakdown
 
