@@ -979,12 +979,18 @@ __global__ void __launch_bounds__(kThreads) k_dist_post(int phase, StateView<T> 
     }
     case DP_POST_NORM: {
       if (gated(h)) return;
-      if (threadIdx.x == 0) {
+      // one warp, the rotation staged in shared memory (givens_column_warp):
+      // on the critical path of every distributed Arnoldi step
+      __shared__ T gsm[3 * kMaxM + 2];
+      if (threadIdx.x < 32) {
         const T hs = sqrt_rn(sv.red[0]);
-        sv.Hc(j, j + 1) = hs;
-        h->h_sub = (double)hs;
         const bool brk = (double)hs <= h->breakdown_tol * h->w0;
-        givens_column(sv, j, h->threshold, brk, m_limit);
+        if (threadIdx.x == 0) {
+          sv.Hc(j, j + 1) = hs;
+          h->h_sub = (double)hs;
+        }
+        __syncwarp();
+        givens_column_warp(sv, j, h->threshold, brk, m_limit, gsm);
       }
       return;
     }
