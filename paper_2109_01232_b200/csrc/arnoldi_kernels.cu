@@ -705,10 +705,13 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
   s = block_sum(s, red);
   const T hs = sqrt_rn(s);
   const bool brk = (double)hs <= sv.h->breakdown_tol * sv.h->w0;   // krylov.py:146
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    sv.Hc(j, j + 1) = hs;
-    sv.h->h_sub = (double)hs;
-    givens_column(sv, j, sv.h->threshold, brk, m_limit);
+  if (blockIdx.x == 0 && threadIdx.x < 32) {   // c2s (>= 3m + 2 elements) is free after the barrier
+    if (threadIdx.x == 0) {
+      sv.Hc(j, j + 1) = hs;
+      sv.h->h_sub = (double)hs;
+    }
+    __syncwarp();
+    givens_column_warp(sv, j, sv.h->threshold, brk, m_limit, c2s);
   }
   if (brk) return;   // no new basis vector on breakdown
   T* vn = const_cast<T*>(V) + (size_t)(j + 1) * ldv;
@@ -1370,6 +1373,9 @@ cudaError_t launch_update_dot_tma(const T* V, long long ldv, long long n, int k,
 // variant at full occupancy.  Returns 0 when no cooperative grid is possible.
 template <typename T>
 struct UnsPlan { unsigned grid = 0; size_t smem = 0; bool cache = false; };
+// leading shared-memory region of K_CS: the c2 coefficients during phase 1,
+// then the warp-staged Givens scratch (>= 3m + 2 elements)
+static inline int kcs_kpad(int m) { return std::max((m + 16) & ~7, (3 * m + 2 + 7) & ~7); }
 
 template <typename T>
 static UnsPlan<T> plan_update_norm_scale(long long n, int m) {
@@ -1382,12 +1388,12 @@ static UnsPlan<T> plan_update_norm_scale(long long n, int m) {
     cudaFuncSetAttribute(k_update_norm_scale<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          dev_smem_optin - 1024);
     cudaFuncSetAttribute(k_update_norm_scale<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (kMaxM + 16) * (int)sizeof(T));
+                         kcs_kpad(kMaxM) * (int)sizeof(T));
     cudaGetLastError();
   });
   UnsPlan<T> p;
   constexpr int VN = Vec<T>::n;
-  const int kpad = (m + 16) & ~7;
+  const int kpad = kcs_kpad(m);
   const size_t base = (size_t)kpad * sizeof(T);
   long long tiles = (n + (long long)kThreads * VN - 1) / ((long long)kThreads * VN);
   if (tiles < 1) tiles = 1;
@@ -1446,7 +1452,7 @@ cudaError_t launch_update_norm_scale(const T* V, long long ldv, long long n, int
     if (e != cudaSuccess) return e;
     return launch_step_scale<T>(w, const_cast<T*>(V) + (size_t)(j + 1) * ldv, n, j, sv, st);
   }
-  const int kpad = (sv.m + 16) & ~7;
+  const int kpad = kcs_kpad(sv.m);
   count_launch();
   const bool pdl = kcs_pdl();
   if (p.cache)
