@@ -314,7 +314,15 @@ def _traffic(cls: str) -> dict:
 
 
 def _backend() -> str:
-    return os.environ.get("MPG_BENCH_BACKEND", "nccl")
+    """NCCL with one GPU per rank; gloo (host-staged collectives, a smoke run of
+    the same path) when ranks outnumber the visible GPUs.  MPG_BENCH_BACKEND
+    overrides."""
+    import torch
+    env = os.environ.get("MPG_BENCH_BACKEND")
+    if env:
+        return env
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    return "gloo" if world > max(1, torch.cuda.device_count()) else "nccl"
 
 
 def dist_arm(args, rank: int, world: int):
