@@ -121,6 +121,21 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   auto bstart = [&](int t) -> long long { return ((long long)blockIdx.x + (long long)t * G) * RB; };
   auto wptr = [&](int t) -> T* { return CACHE ? wsm + (size_t)t * RB : wg + bstart(t); };
 
+  // P1 streams x alone (latency-bound, HBM mostly idle): stage the first
+  // MPG_MEGA_PF1 blocks of each group's pass-1 dot sweep into L2 meanwhile
+#ifndef MPG_MEGA_PF1
+#define MPG_MEGA_PF1 8
+#endif
+  if (MPG_MEGA_PF1 > 0) {
+    for (int idx = lane; idx < KV * MPG_MEGA_PF1; idx += 32) {
+      const int q = idx % KV, d = idx / KV;
+      const int t = grp + d * kMegaGroups;
+      const long long b0 = bstart(t);
+      if (gw + 8 * q < k && t < nb && b0 + RB <= n)
+        prefetch_l2_bulk(V + (size_t)(gw + 8 * q) * ldv + b0, RB * sizeof(T));
+    }
+  }
+
   // ---------------------------------------------------------------- P1 SpMV
   long long off[S];
   {
