@@ -241,9 +241,16 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   }
   // the basis blocks P2 starts with do not depend on c1: stage them into L2
   // while the grid waits at B1
-  if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k && grp < nb) {
-    const long long b0 = bstart(grp);
-    if (b0 + RB <= n) prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + b0, RB * sizeof(T));
+#ifndef MPG_MEGA_PFB
+#define MPG_MEGA_PFB 1
+#endif
+  if (MPG_MEGA_PF && lane < KV && gw + 8 * lane < k) {
+#pragma unroll
+    for (int d = 0; d < MPG_MEGA_PFB; ++d) {
+      const long long b0 = bstart(grp + d * kMegaGroups);
+      if (grp + d * kMegaGroups < nb && b0 + RB <= n)
+        prefetch_l2_bulk(V + (size_t)(gw + 8 * lane) * ldv + b0, RB * sizeof(T));
+    }
   }
   MEGA_STAMP(2)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B1
@@ -357,9 +364,12 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     for (int g = 0; g < kMegaGroups; ++g) t += cred[g][tid];
     part[(size_t)(kColDot2 + tid) * kMaxParts + blockIdx.x] = t;
   }
-  if (MPG_MEGA_PF && lane < k && warp < nb) {   // P3's first block per warp, likewise
-    const long long b0 = bstart(warp);
-    if (b0 + RB <= n) prefetch_l2_bulk(V + (size_t)lane * ldv + b0, RB * sizeof(T));
+  if (MPG_MEGA_PF && lane < k) {   // P3's first block(s) per warp, likewise
+#pragma unroll
+    for (int d = 0; d < MPG_MEGA_PFB; ++d) {
+      const long long b0 = bstart(warp + d * kMegaWarps);
+      if (warp + d * kMegaWarps < nb && b0 + RB <= n) prefetch_l2_bulk(V + (size_t)lane * ldv + b0, RB * sizeof(T));
+    }
   }
   MEGA_STAMP(4)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B2
