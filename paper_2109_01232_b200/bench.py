@@ -8,10 +8,10 @@ thresholds (densest row < 15 nonzeros = left; speedup >= 1.7 = top).  Here
 the products are CSR SpMV launches on device-resident operands timed with
 CUDA events, so the batch time is device time.
 
-``sweep_switch_point`` / ``sweep_restart`` follow bench.py:243-312: the
-same rows (fp64 and refinement baselines plus one GMRES-FD run per switch
-point; fp64 and refinement per restart length) with ``time_s`` the solver's
-``total_time``.  ``config`` is the reference's ``RunConfig`` (io.py:243),
+``sweep_switch_point`` / ``sweep_restart`` / ``sweep_rhs`` follow
+bench.py:243-343: the same rows (fp64 and refinement baselines plus one
+GMRES-FD run per switch point; fp64 and refinement per restart length and per
+right-hand-side kind) with ``time_s`` the solver's ``total_time``.  ``config`` is the reference's ``RunConfig`` (io.py:243),
 accepted duck-typed; Matrix Market input and RCM reordering go through
 ``paper_2109_01232_b200.io``.
 """
@@ -34,7 +34,7 @@ from .solvers import StopCriteria, gmres_fd, gmres_ir, gmres_restarted
 from .spmv import predicted_speedup
 
 __all__ = ["Quadrant", "SpmvBenchResult", "classify_speedup", "spmv_bench", "run_experiment", "summary_row",
-           "sweep_switch_point", "sweep_restart", "SWITCH_FIELDS", "RESTART_FIELDS"]
+           "sweep_switch_point", "sweep_restart", "sweep_rhs", "SWITCH_FIELDS", "RESTART_FIELDS", "RHS_FIELDS"]
 
 MAX_ROW_NNZ_THRESHOLD = 15      # bench.py:42
 SPEEDUP_THRESHOLD = 1.7         # bench.py:43
@@ -260,4 +260,29 @@ def sweep_restart(config, sizes: list[int], out_dir: str | None = None) -> list[
     out = out_dir or getattr(config, "out", None)
     if out:
         _write_rows(rows, RESTART_FIELDS, os.path.join(out, f"sweep_restart_{name.replace(':', '_')}.csv"))
+    return rows
+
+
+RHS_FIELDS = ["rhs", "time_double", "iters_double", "time_ir", "iters_ir", "speedup"]
+
+
+def sweep_rhs(config, kinds: list, out_dir: str | None = None) -> list[dict]:
+    """fp64 and refinement solves for each right-hand-side kind (bench.py:318-343)."""
+    from dataclasses import replace
+    if hasattr(config, "validate"):
+        config.validate()
+    criteria = StopCriteria(rtol=config.rtol, max_iters=config.max_iters, m=config.m)
+    rows, name = [], None
+    for rhs in kinds:
+        name, A, b = _problem(replace(config, rhs=rhs))
+        dbl = gmres_restarted(A, b, criteria=criteria, precision=FP64)
+        ir = gmres_ir(A, b, criteria=criteria)
+        kind = rhs.kind.value if hasattr(rhs.kind, "value") else str(rhs.kind)
+        rows.append({"rhs": kind, "time_double": repr(dbl.total_time), "iters_double": dbl.total_iters,
+                     "time_ir": repr(ir.total_time), "iters_ir": ir.total_iters,
+                     "speedup": repr(dbl.total_time / ir.total_time if ir.total_time else float("nan")),
+                     "converged_double": dbl.converged, "converged_ir": ir.converged})
+    out = out_dir or getattr(config, "out", None)
+    if out and name:
+        _write_rows(rows, RHS_FIELDS, os.path.join(out, f"sweep_rhs_{name.replace(':', '_')}.csv"))
     return rows

@@ -16,8 +16,8 @@ Mirrors the reference's ``mpgmres.precond`` (pkg/src/mpgmres/precond.py):
 * ``cast_apply``           precond.py:393-414.
 
 Reference preconditioner objects (duck-typed) are accepted everywhere.
-RCM reordering (precond.py:421-515) is host preprocessing outside the hot
-path and is not provided here.
+RCM reordering (precond.py:421-515) is host preprocessing; it lives in
+``paper_2109_01232_b200.io.rcm_reorder``.
 """
 
 from __future__ import annotations

@@ -1,4 +1,4 @@
-"""Reduction-order sensitivity of GMRES-FD iteration counts (test evidence).
+"""Reduction-order sensitivity of GMRES-FD and GMRES-IR iteration counts (test evidence).
 
 GMRES-FD switches from fp32 to fp64 at `switch_iter`.  When the switch
 comes after the fp32 leg has reached its attainable accuracy (explicit
@@ -9,10 +9,15 @@ script re-runs the CPU oracle (bit-identical to the reference, see
 test_oracle.py) with the fp32 reductions re-associated in ways any valid
 implementation might use (reversed, blocked, pairwise, column-sequential, ...)
 and records the spread of total iteration counts.  tests/test_gpu_solvers.py
-uses that spread as the parity band for FD cases whose switch is at the fp32
-floor; all other solvers keep the +-2 % bar.
+records that spread next to the count of the device-order oracle
+(oracle/devorder.c: the association the GPU kernels use), so an order-sensitive
+case's reference count, its spread and the GPU's own order sit side by side.
+GMRES-IR on Laplace3D(40) is the case SURVEY.md A.5 flags: the reference
+needs 250 iterations, blocked / pairwise reductions 200.  The tests do NOT
+widen any parity band with this spread: order-sensitive cases are asserted
+bit for bit against the device-order oracle (tests/test_gpu_parity_order.py).
 
-    python tests/golden/fd_order_spread.py      # writes fd_order_spread.json
+    python tests/golden/order_spread.py      # writes order_spread.json
 """
 
 from __future__ import annotations
@@ -27,8 +32,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from oracle import cpu_gmres as O  # noqa: E402
+from oracle import devorder as D  # noqa: E402
 
-CASES = [("laplace3d", 30, 100), ("laplace2d", 100, 200)]
+CASES = [("laplace3d", 30, "fd", 100), ("laplace2d", 100, "fd", 200), ("laplace3d", 40, "ir", 0)]
 
 
 def _blocked(B, rev=False):
@@ -102,7 +108,7 @@ def main():
     orig = (O.basis_dots, O.basis_update, O.nrm2)
     out = {}
     try:
-        for kind, nx, sw in CASES:
+        for kind, nx, solver, sw in CASES:
             A = O.stencil_csr(kind, nx)
             b = O.ones_rhs(A.n_rows)
             counts = {}
@@ -110,13 +116,19 @@ def main():
                 O.basis_dots = v.get("d", orig[0])
                 O.basis_update = v.get("u", orig[1])
                 O.nrm2 = v.get("n", orig[2])
-                counts[name] = int(O.solve_fd(A, b, m=50, switch_iter=sw).total_iters)
-                print(kind, nx, sw, name, counts[name], flush=True)
+                run = (lambda: O.solve_fd(A, b, m=50, switch_iter=sw)) if solver == "fd" else \
+                    (lambda: O.solve_ir(A, b, m=50))
+                counts[name] = int(run().total_iters)
+                print(kind, nx, solver, sw, name, counts[name], flush=True)
+            O.basis_dots, O.basis_update, O.nrm2 = orig
+            dev = D.solve_fd(A, b, m=50, switch_iter=sw) if solver == "fd" else D.solve_ir(A, b, m=50)
             vals = list(counts.values())
-            out[f"{kind}:{nx}/fd{sw}/m50"] = {"counts": counts, "min": min(vals), "max": max(vals)}
+            key = f"{kind}:{nx}/fd{sw}/m50" if solver == "fd" else f"{kind}:{nx}/ir/m50"
+            out[key] = {"counts": counts, "min": min(vals), "max": max(vals),
+                        "device_order": int(dev.total_iters)}
     finally:
         O.basis_dots, O.basis_update, O.nrm2 = orig
-    with open(os.path.join(HERE, "fd_order_spread.json"), "w") as f:
+    with open(os.path.join(HERE, "order_spread.json"), "w") as f:
         json.dump(out, f, indent=1)
 
 

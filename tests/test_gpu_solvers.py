@@ -25,36 +25,25 @@ def within_2pct(got, want):
     return abs(got - want) <= max(0.02 * want, 0)
 
 
-def _fd_spread():
+def _order_study():
     import json, os
-    with open(os.path.join(os.path.dirname(__file__), "golden", "fd_order_spread.json")) as f:
+    with open(os.path.join(os.path.dirname(__file__), "golden", "order_spread.json")) as f:
         return json.load(f)
 
 
-FD_SPREAD = _fd_spread()
+ORDER_STUDY = _order_study()
 
 
 def iters_match(rep, g, m, rtol=1e-10, name=None):
-    """+-2 % of the reference count, or — IR counts being quantised to whole
-    restart cycles — exactly one cycle off where the crossing
+    """+-2 % of the reference count, or -- IR counts being quantised to whole
+    restart cycles -- exactly one cycle off where the crossing
     is marginal: the side that did not converge at that boundary was within
-    2x of rtol there.  Anything else is a parity failure."""
+    2x of rtol there.  Anything else is a parity failure.  (Cases whose count
+    depends on the reduction order beyond this, e.g. laplace3d:40 GMRES-IR,
+    are judged by ORDER_SENSITIVE below instead.)"""
     got, want = rep.total_iters, g["total_iters"]
     if within_2pct(got, want):
         return True
-    # GMRES-FD with the switch after the fp32 leg has reached its attainable
-    # accuracy (explicit residual ~1e-5 at the switch): the fp64 leg restarts
-    # from an iterate whose error is the fp32 leg's accumulated rounding, so its
-    # length depends on the ORDER of the fp32 reductions.  The reference itself
-    # spans [min, max] under valid re-associations of those sums
-    # (tests/golden/fd_order_spread.py, e.g. 186..197 for laplace3d:30/fd100);
-    # accept the reference count +- twice that spread, and the fp32 leg exact.
-    if g.get("iters_fp32", 0) > 0 and g.get("iters_fp64", 0) > 0:
-        if rep.iters_fp32 != g["iters_fp32"]:
-            return False
-        sp = FD_SPREAD.get(name)
-        band = 2 * (sp["max"] - sp["min"]) if sp else 0
-        return abs(got - want) <= max(0.02 * want, band)
     if abs(got - want) != m:
         return False
     if got < want:   # we converged one cycle earlier than the reference
@@ -62,6 +51,17 @@ def iters_match(rep, g, m, rtol=1e-10, name=None):
         return ref_marks.get(got, 1.0) <= 2 * rtol
     ours = {e.iteration: e.explicit for e in rep.residual_history if e.explicit is not None}
     return ours.get(want, 1.0) <= 2 * rtol
+
+
+# Cases whose iteration count is decided by the association of the fp32 dot
+# products: the reference needs 250 iterations for
+# laplace3d:40 GMRES-IR, while blocked / pairwise / device-ordered sums of the
+# same algorithm need 200 (tests/golden/order_spread.json).  For these the bar
+# is the device-order oracle (oracle/devorder.c, the reference's algorithm
+# with the kernels' association): the GPU solve must equal it BIT FOR BIT, and
+# the oracle must reproduce the reference count with the reference's own
+# order (test_oracle.py).  No band is widened.
+ORDER_SENSITIVE = {"laplace3d:40/ir/m50"}
 
 
 def rel_err(x, y):
@@ -80,11 +80,16 @@ SOLVER_CASES = [
     ("laplace2d:100/fp64/m100", "laplace2d", 100, {}, "fp64", {"m": 100}),
     ("laplace2d:100/ir/m100", "laplace2d", 100, {}, "ir", {"m": 100}),
     ("laplace3d:40/fp64/m50", "laplace3d", 40, {}, "fp64", {"m": 50}),
+    ("laplace3d:40/ir/m50", "laplace3d", 40, {}, "ir", {"m": 50}),
     ("laplace3d:30/fd100/m50", "laplace3d", 30, {}, "fd", {"m": 50, "switch_iter": 100}),
     ("convdiff2d:100:c100/fp64/m50", "convdiff2d", 100, {"convection": 100.0}, "fp64", {"m": 50}),
     ("convdiff2d:100:c100/ir/m50", "convdiff2d", 100, {"convection": 100.0}, "ir", {"m": 50}),
     ("recirc2d:40:c0.5/ir/m50", "recirc2d", 40, {"convection": 0.5}, "ir", {"m": 50}),
 ]
+
+
+def _nsm():
+    return torch.cuda.get_device_properties(0).multi_processor_count
 
 
 def run(A, b, solver, extra):
@@ -119,7 +124,14 @@ def test_solver_parity(case, golden_runs):
     rep = run(dev(Ao), b, solver, extra)
     g = golden_runs[name]
     assert rep.converged == g["converged"]
-    assert iters_match(rep, g, extra["m"], name=name), (rep.total_iters, g["total_iters"], g["boundaries"][-3:])
+    if name in ORDER_SENSITIVE:
+        from oracle import devorder as D
+        dv = {"ir": D.solve_ir, "fp64": D.solve_restarted}[solver](Ao, b, m=extra["m"], nsm=_nsm())
+        assert rep.total_iters == dv.total_iters and np.array_equal(rep.x, dv.x), (rep.total_iters, dv.total_iters)
+        study = ORDER_STUDY[name]
+        assert study["device_order"] == dv.total_iters and study["counts"]["reference"] == g["total_iters"]
+    else:
+        assert iters_match(rep, g, extra["m"], name=name), (rep.total_iters, g["total_iters"], g["boundaries"][-3:])
     orep = oracle_run(Ao, b, solver, extra)
     assert orep.total_iters == g["total_iters"]          # oracle pinned to the reference
     assert rel_err(rep.x, orep.x) <= 1e-8
@@ -380,14 +392,17 @@ def test_cfg3_convdiff1500_full_solve_vs_reference(solver, cfg3_reference):
     assert np.linalg.norm(x - ref) / np.linalg.norm(ref) <= 1e-8
 
 
-@pytest.mark.parametrize("kind,nx,kw,solver", [("laplace3d", 40, {}, "ir"), ("laplace3d", 40, {}, "fp64"),
-                                               ("laplace2d", 100, {}, "ir"),
-                                               ("convdiff2d", 100, {"convection": 100.0}, "fp64")])
-def test_persistent_step_kernel_matches_split_step(kind, nx, kw, solver):
+@pytest.mark.parametrize("name,kind,nx,kw,solver", [
+    ("laplace3d:40/ir/m50", "laplace3d", 40, {}, "ir"), ("laplace3d:40/fp64/m50", "laplace3d", 40, {}, "fp64"),
+    ("laplace2d:100/ir/m50", "laplace2d", 100, {}, "ir"),
+    ("convdiff2d:100:c100/fp64/m50", "convdiff2d", 100, {"convection": 100.0}, "fp64")])
+def test_persistent_step_kernel_matches_split_step(name, kind, nx, kw, solver, golden_runs):
     """The persistent per-step kernel (csrc/step_kernel.cu) and the four-launch
-    step compute the same CGS2 step with differently ordered reductions: same
-    iteration counts (parity rule), solutions within 1e-10, both at the
-    reference's counts."""
+    step compute the same CGS2 step with differently ordered reductions.  Both
+    must converge at the reference's count (iters_match) -- or, for the
+    order-sensitive laplace3d:40 GMRES-IR, at the device-order count, the
+    persistent one bit for bit -- with solutions within 1e-9 of each other and
+    final fp64 residuals <= rtol."""
     A = P.generate(P.StencilSpec(P.StencilKind(kind), nx, **kw))
     b = np.ones(A.n_rows)
     crit = P.StopCriteria(rtol=1e-10, m=50)
@@ -396,11 +411,21 @@ def test_persistent_step_kernel_matches_split_step(kind, nx, kw, solver):
         r1 = f(A, b, criteria=crit)
     with P.solvers.step_kernel("persistent"):
         r2 = f(A, b, criteria=crit)
-    assert r2.converged and abs(r1.total_iters - r2.total_iters) <= max(1, int(0.02 * r1.total_iters)) or \
-        abs(r1.total_iters - r2.total_iters) == 50
+    g = golden_runs[name]
+    assert r1.converged and r2.converged
+    if name in ORDER_SENSITIVE:
+        from oracle import devorder as D
+        Ao = O.stencil_csr(kind, nx, **kw)
+        dv = D.solve_ir(Ao, b, m=50, nsm=_nsm())
+        assert r2.total_iters == dv.total_iters and np.array_equal(r2.x, dv.x)
+        assert r1.total_iters == dv.total_iters, (r1.total_iters, dv.total_iters)
+    else:
+        assert iters_match(r1, g, 50), (r1.total_iters, g["total_iters"])
+        assert iters_match(r2, g, 50), (r2.total_iters, g["total_iters"])
     assert rel_err(r2.x, r1.x) <= 1e-9
-    rn, _ = P.explicit_residual(A, b, r2.x)
-    assert rn / np.linalg.norm(b) <= 1e-10
+    for r in (r1, r2):
+        rn, _ = P.explicit_residual(A, b, r.x)
+        assert rn / np.linalg.norm(b) <= 1e-10
 
 
 @pytest.fixture(scope="module")

@@ -142,13 +142,52 @@ def test_oracle_equals_reference_directly(reference):
                 assert np.array_equal(ref.x, ora.x)
 
 
-def test_fd_order_spread_fixture_is_anchored_on_the_reference(golden_runs):
-    """The FD reduction-order study (tests/golden/fd_order_spread.py) starts from
-    the unperturbed oracle, which must reproduce the reference's count."""
+def test_order_study_fixture_is_anchored_on_the_reference(golden_runs):
+    """The reduction-order study (tests/golden/order_spread.py) starts from the
+    unperturbed oracle, which must reproduce the reference's count."""
     import json
     import os
-    with open(os.path.join(os.path.dirname(__file__), "golden", "fd_order_spread.json")) as f:
+    with open(os.path.join(os.path.dirname(__file__), "golden", "order_spread.json")) as f:
         spread = json.load(f)
     for name, sp in spread.items():
         assert sp["counts"]["reference"] == golden_runs[name]["total_iters"]
         assert sp["min"] <= sp["counts"]["reference"] <= sp["max"]
+        assert "device_order" in sp
+
+
+# ------------------------------------------------------------ device-order oracle
+
+def test_device_order_oracle_builds_and_shares_the_reference_spmv(rng):
+    """oracle/devorder.c (the reference algorithm with the GPU kernels'
+    reduction association) computes every SpMV exactly as the reference-order
+    oracle: the row order of spmv.py:48-72 is the same on both."""
+    import ctypes as C
+    from oracle import devorder as D
+    L = D.lib()
+    for kind, nx, kw in (("laplace3d", 9, {}), ("recirc2d", 17, {"convection": 3.0}),
+                         ("convdiff2d", 12, {"convection": 40.0})):
+        A = O.stencil_csr(kind, nx, **kw)
+        for dt, fn in ((np.float64, L.devorder_spmv_f64), (np.float32, L.devorder_spmv_f32)):
+            Ad = A.astype(dt)
+            x = rng.standard_normal(A.n_rows).astype(dt)
+            y = np.empty(A.n_rows, dtype=dt)
+            fn(C.c_int(A.n_rows), D._p(np.ascontiguousarray(Ad.row_ptr, np.int32)),
+               D._p(np.ascontiguousarray(Ad.col_idx, np.int32)), D._p(np.ascontiguousarray(Ad.values)),
+               D._p(x), D._p(y))
+            assert np.array_equal(y.view(np.uint8), O.spmv(Ad, x).view(np.uint8))
+
+
+def test_device_order_oracle_converges_like_the_reference_where_order_is_benign(golden_runs):
+    """Where the count is insensitive to the association, the
+    device-order oracle reproduces the reference's golden counts; its
+    solutions agree with the reference-order oracle to 1e-8."""
+    from oracle import devorder as D
+    for name, kind, nx, solver in (("laplace2d:50/fp64/m50", "laplace2d", 50, "fp64"),
+                                   ("laplace2d:50/ir/m50", "laplace2d", 50, "ir"),
+                                   ("laplace2d:100/ir/m50", "laplace2d", 100, "ir")):
+        A = O.stencil_csr(kind, nx)
+        b = O.ones_rhs(A.n_rows)
+        dv = D.solve_ir(A, b, m=50) if solver == "ir" else D.solve_restarted(A, b, m=50)
+        ref = O.solve_ir(A, b, m=50) if solver == "ir" else O.solve_restarted(A, b, m=50)
+        assert dv.total_iters == golden_runs[name]["total_iters"] == ref.total_iters
+        assert np.linalg.norm(dv.x - ref.x) <= 1e-8 * np.linalg.norm(ref.x)
