@@ -197,7 +197,8 @@ typedef struct {
   int32_t breakdown;  /* last step hit the breakdown test */
   int32_t m;          /* capacity */
   int32_t prec;
-  int32_t reserved0, reserved1;
+  int32_t kt_cat;     /* device kernel timing: category of the running interval (-1 none) */
+  int32_t reserved1;  /* distributed peer halo: sequence number */
   double gamma;         /* ||r0|| of the cycle, working precision value */
   double b_norm;        /* b_norm of the cycle's threshold */
   double threshold;     /* rtol * b_norm */
@@ -208,7 +209,16 @@ typedef struct {
   double w0;            /* pre-orthogonalisation norm of the last step */
   double h_sub;         /* last subdiagonal entry */
   double outer_b_norm;  /* ||b|| of the outer problem (written by mpg_solver_begin) */
-  double reserved[6];
+  double reserved[1];   /* distributed mode: raw local sums of the norm phases */
+  /* Device time per kernel category (the reference's KernelTimer bins,
+   * timing.py:17-23): [0] SpMV, [1] GemvTrans, [2] Norm, [3] GemvNoTrans, in
+   * globaltimer nanoseconds, accumulated since mpg_solver_begin.  Each kernel
+   * of a cycle stamps %globaltimer once in CTA 0 at entry (the persistent
+   * step also at its internal grid barriers); the interval up to the next
+   * stamp is charged to the category the stamp opened (Other is not stored:
+   * the host takes it as total - sum, timing.py:44-47). */
+  uint64_t ktime_ns[4];
+  uint64_t kt_mark;     /* globaltimer of the last stamp */
 } mpg_state_header;
 
 /* Total bytes of a cycle state for restart length m in precision prec. */

@@ -37,11 +37,12 @@ class CudaCallError(RuntimeError):
 class StateHeader(C.Structure):
     _fields_ = [("flags", C.c_int32), ("steps", C.c_int32), ("done", C.c_int32),
                 ("breakdown", C.c_int32), ("m", C.c_int32), ("prec", C.c_int32),
-                ("reserved0", C.c_int32), ("reserved1", C.c_int32),
+                ("kt_cat", C.c_int32), ("reserved1", C.c_int32),
                 ("gamma", C.c_double), ("b_norm", C.c_double), ("threshold", C.c_double),
                 ("rnorm", C.c_double), ("rho", C.c_double), ("rtol", C.c_double),
                 ("breakdown_tol", C.c_double), ("w0", C.c_double), ("h_sub", C.c_double),
-                ("outer_b_norm", C.c_double), ("reserved", C.c_double * 6)]
+                ("outer_b_norm", C.c_double), ("reserved", C.c_double * 1),
+                ("ktime_ns", C.c_uint64 * 4), ("kt_mark", C.c_uint64)]
 
 
 class PolyOp(C.Structure):

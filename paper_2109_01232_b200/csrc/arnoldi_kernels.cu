@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(kUdThreads) k_update_dot(const T* __restrict__
                                                            StateView<T> sv, WsView ws, int TB,
                                                            int S) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_TN);
   extern __shared__ __align__(128) unsigned char smraw[];
   const size_t stage_elems = (size_t)(k + 1) * TB;
   T* stages = reinterpret_cast<T*>(smraw);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, MPG_KB_MINB) k_update_dot_w(const T*
   pdl_wait();
   pdl_trigger();
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_TN);
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
   constexpr int RPW = RB / kWarps;   // rows each warp reduces per block
@@ -274,6 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_dot1_w(const T* __restrict__ w, lo
                                                      const T* __restrict__ V, long long ldv, int k,
                                                      StateView<T> sv, WsView ws) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_T);
   constexpr int VN = Vec<T>::n;
   __shared__ T red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -331,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, MPG_KA2_MINB) k_dot1_wo(const T* __r
   pdl_wait();
   pdl_trigger();
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_T);
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
   __shared__ T red[32];
@@ -434,6 +438,7 @@ __global__ void __launch_bounds__(kThreads) k_dot1_small(const T* __restrict__ w
   pdl_wait();
   pdl_trigger();
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_T);
   constexpr int VN = Vec<T>::n;
   __shared__ T red8[(KT + 2) * kWarps];
   T acc[KT + 2];
@@ -491,6 +496,7 @@ __global__ void __launch_bounds__(kThreads) k_update_dot_small(const T* __restri
   pdl_wait();
   pdl_trigger();
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_TN);
   constexpr int VN = Vec<T>::n;
   __shared__ T red8[KT * kWarps];
   T c1q[KT], acc[KT];
@@ -543,6 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_update_norm(const T* __restrict__ 
                                                           long long n, int j, T* __restrict__ w,
                                                           StateView<T> sv, WsView ws, int m_limit) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_N);
   constexpr int VN = Vec<T>::n;
   const int k = j + 1;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -613,6 +620,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) k_step_scale(const T* __restrict__ w, T* __restrict__ vn,
                                                          long long n, int j, StateView<T> sv) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_OTHER);
   constexpr int VN = Vec<T>::n;
   const T hs = sv.Hc(j, j + 1);
   const long long nv = n / VN;
@@ -648,6 +656,7 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
   pdl_wait();
   pdl_trigger();
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_GEMV_N);
   constexpr int VN = Vec<T>::n;
   const int k = j + 1;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -698,12 +707,14 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
   const T t = block_sum(ss, red);
   T* part = static_cast<T*>(ws.part);
   if (threadIdx.x == 0) part[blockIdx.x] = t;
+  if (blockIdx.x == 0 && threadIdx.x == 0) kt_stamp(sv.h, KC_NORM);   // barrier + norm tail
   grid_barrier(ws.counter, ws.counter + 1);
   // the same fixed-order sum in every CTA (identical to k_update_norm's last CTA)
   T s = T(0);
   for (int p = threadIdx.x; p < (int)gridDim.x; p += blockDim.x) s += __ldcg(part + p);
   s = block_sum(s, red);
   const T hs = sqrt_rn(s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) kt_stamp(sv.h, KC_OTHER);  // Givens + v = w / h
   const bool brk = (double)hs <= sv.h->breakdown_tol * sv.h->w0;   // krylov.py:146
   if (blockIdx.x == 0 && threadIdx.x < 32) {   // c2s (>= 3m + 2 elements) is free after the barrier
     if (threadIdx.x == 0) {
@@ -749,6 +760,7 @@ __global__ void __launch_bounds__(kThreads) k_step_scale_peer(const T* __restric
                                                               uint32_t* prev_flag, uint32_t* next_flag,
                                                               unsigned int* counter) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_OTHER);
   const T hs = sv.Hc(j, j + 1);
   for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
        r += (long long)gridDim.x * blockDim.x) {
@@ -860,6 +872,7 @@ __global__ void __launch_bounds__(kThreads) k_start(const T* __restrict__ r0, lo
                                                     StateView<T> sv, double rtol,
                                                     const double* b_norm_src, double btol,
                                                     WsView ws) {
+  kt_mark(sv.h, KC_NORM);
   __shared__ T red[32];
   T ss = T(0);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -892,6 +905,7 @@ __global__ void __launch_bounds__(kThreads) k_start_ir(const double* __restrict_
                                                        float* __restrict__ r32, long long n,
                                                        StateView<float> sv, double rtol,
                                                        double btol, WsView ws) {
+  kt_mark(sv.h, KC_OTHER);
   __shared__ float red[32];
   __shared__ int ovf_s;
   const double rho = sv.h->rnorm;
@@ -934,6 +948,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) k_start_scale(const T* __restrict__ r0, T* __restrict__ v0,
                                                           long long n, StateView<T> sv) {
   if (gated(sv.h)) return;
+  kt_mark(sv.h, KC_OTHER);
   const T gamma = sv.g[0];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -1025,6 +1040,7 @@ template cudaError_t launch_dist_post<double>(int, StateView<double>, int, int, 
 // column order).  One warp.
 template <typename T>
 __global__ void k_lsq(StateView<T> sv) {
+  kt_mark(sv.h, KC_OTHER);
   const int k = sv.h->steps;
   const int lane = threadIdx.x;
   if (k == 0 || (sv.h->flags & (MPG_FLAG_NONFINITE_OP | MPG_FLAG_NONFINITE_GAMMA | MPG_FLAG_OVERFLOW)))
@@ -1057,6 +1073,7 @@ template <typename T, typename TX, int MODE>
 __global__ void __launch_bounds__(kThreads) k_combine(const T* __restrict__ V, long long ldv,
                                                       long long n, StateView<T> sv, TX* x,
                                                       const void* diag, T* u) {
+  kt_mark(sv.h, KC_GEMV_N);
   const int k = sv.h->steps;
   if (k == 0 || (sv.h->flags & (MPG_FLAG_NONFINITE_OP | MPG_FLAG_NONFINITE_GAMMA |
                                  MPG_FLAG_OVERFLOW | MPG_FLAG_SINGULAR)))

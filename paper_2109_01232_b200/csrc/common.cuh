@@ -328,6 +328,42 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Device kernel-time attribution (the reference's KernelTimer categories,
+// timing.py:17-23; header fields ktime_ns / kt_mark / kt_cat).  CTA 0 thread 0
+// of each kernel of a cycle stamps %globaltimer once at entry; the interval
+// since the previous stamp is charged to the category that stamp opened.
+// Kernels on a stream run in order, so one thread per kernel suffices and no
+// atomics are needed.  KC_OTHER is not stored (host: total - sum).
+enum KtCat { KC_SPMV = 0, KC_GEMV_T = 1, KC_NORM = 2, KC_GEMV_N = 3, KC_OTHER = 4,
+             KC_GEMV_TN = 5 /* fused update + dots: half GemvNoTrans, half GemvTrans */ };
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Unconditional stamp (the caller picks the thread).
+__device__ __forceinline__ void kt_stamp(const mpg_state_header* hc, int cat) {
+  mpg_state_header* h = const_cast<mpg_state_header*>(hc);
+  const unsigned long long now = gtimer_ns();
+  const int prev = h->kt_cat;
+  const unsigned long long d = now - h->kt_mark;
+  if (h->kt_mark == 0) {
+    // first stamp since the reset (mpg_solver_begin / a zeroed state): opens only
+  } else if (prev >= 0 && prev < 4) {
+    h->ktime_ns[prev] += d;
+  } else if (prev == KC_GEMV_TN) {
+    h->ktime_ns[KC_GEMV_N] += d / 2;
+    h->ktime_ns[KC_GEMV_T] += d - d / 2;
+  }
+  h->kt_mark = now;
+  h->kt_cat = cat;
+}
+// Kernel-entry stamp: CTA 0, thread 0; null header = untimed launch.
+__device__ __forceinline__ void kt_mark(const mpg_state_header* h, int cat) {
+  if (h != nullptr && blockIdx.x == 0 && threadIdx.x == 0) kt_stamp(h, cat);
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const TS* __restrict__ x, 
                                                       long long n, int64_t* ovf,
                                                       const mpg_state_header* gate) {
   if (gate_done(gate)) return;
+  kt_mark(gate, KC_OTHER);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const TS v = x[i];
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kThreads) k_finish_add(TX* x, const T* __restr
                                                          long long n, const mpg_state_header* gate,
                                                          int ir) {
   if (gate->steps == 0) return;
+  kt_mark(gate, KC_OTHER);
   if (gate->flags & (MPG_FLAG_NONFINITE_OP | MPG_FLAG_NONFINITE_GAMMA | MPG_FLAG_OVERFLOW |
                      MPG_FLAG_SINGULAR))
     return;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(kThreads) k_poly_elem(int op, T a, const T* __
                                                         T* dst, T* y, long long n,
                                                         const mpg_state_header* gate) {
   if (gate_done(gate)) return;
+  kt_mark(gate, KC_OTHER);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     if (op == MPG_POLY_SCALE) dst[i] = mul_rn(a, src[i]);
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi1(const T* __restrict__ d, c
                                                       T* __restrict__ y, long long n,
                                                       const mpg_state_header* gate) {
   if (gate_done(gate)) return;
+  kt_mark(gate, KC_OTHER);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = div_rn(x[i], d[i]);   // xb[:, 0] /= lu[:, 0, 0]
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) k_jacobi_blocks(const T* __restrict_
                                                             long long n, int k,
                                                             const mpg_state_header* gate) {
   if (gate_done(gate)) return;
+  kt_mark(gate, KC_OTHER);
   const long long nb = (n + k - 1) / k;
   T xb[kMaxJacobiBlock];
   for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nb;

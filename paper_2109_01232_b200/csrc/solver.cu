@@ -68,18 +68,21 @@ static cudaError_t with_matrix(const mpg_solver_desc& d, const TP* csr_vals, con
 // :205, :330, :358): fp64 for GMRES-IR and fp64 GMRES, fp32 for the fp32 solver.
 static cudaError_t outer_residual(const mpg_solver_desc& d, WsView ws, cudaStream_t st) {
   mpg_state_header* h = hdr_of(d);
+  // GMRES-IR's refinement residual is "Other" (timing.suspended, solvers.py:328,356);
+  // the restarted solvers bin theirs as SpMV (solvers.py:186,205 through spmv)
+  const int kcat = d.mode == MPG_MODE_IR ? KC_OTHER : KC_SPMV;
   if (d.mode == MPG_MODE_IR || d.prec == MPG_FP64) {
     const double* vals = d.mode == MPG_MODE_IR ? d.values64 : static_cast<const double*>(d.values);
     const void* dia = d.mode == MPG_MODE_IR ? static_cast<const void*>(d.dia64) : d.dia;
     return with_matrix<double>(d, vals, dia, [&](const auto& A) {
       return launch_residual<double>(A, static_cast<const double*>(d.b),
                                      static_cast<const double*>(d.x), static_cast<double*>(d.r),
-                                     nullptr, h, ws, st);
+                                     nullptr, h, ws, st, 0, h, kcat);
     });
   }
   return with_matrix<float>(d, static_cast<const float*>(d.values), d.dia, [&](const auto& A) {
     return launch_residual<float>(A, static_cast<const float*>(d.b), static_cast<const float*>(d.x),
-                                  static_cast<float*>(d.r), nullptr, h, ws, st);
+                                  static_cast<float*>(d.r), nullptr, h, ws, st, 0, h, kcat);
   });
 }
 
@@ -104,6 +107,7 @@ template <typename TP>
 static cudaError_t run_poly(const mpg_solver_desc& d, const std::vector<mpg_poly_op>& ops,
                             const TP* vals, const TP* x, TP* y, TP* t0, TP* t1, TP* t2,
                             const mpg_state_header* gate, WsView ws, cudaStream_t st) {
+  const mpg_state_header* kt = hdr_of(d);   // its SpMVs are binned SpMV (precond.py:300-319)
   TP* bufs[5] = {const_cast<TP*>(x), y, t0, t1, t2};
   for (const mpg_poly_op& op : ops) {
     switch (op.op) {
@@ -114,7 +118,7 @@ static cudaError_t run_poly(const mpg_solver_desc& d, const std::vector<mpg_poly
         break;
       default:
         TRY(with_matrix<TP>(d, vals, d.pc_dia, [&](const auto& A) {
-          return launch_poly_op<TP>(A, op, x, y, t0, t1, t2, gate, d.n, ws, st);
+          return launch_poly_op<TP>(A, op, x, y, t0, t1, t2, gate, d.n, ws, st, kt);
         }));
     }
   }
@@ -273,7 +277,7 @@ static cudaError_t enqueue_cycle(const mpg_solver& s, int m_limit, cudaStream_t 
     if (split_spmv_dot1()) {
       {
         ProfScope ps(PK_SPMV_DOT);
-        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st); }));
+        TRY(with_matrix<T>(d, vals, d.dia, [&](const auto& A) { return launch_spmv<T>(A, z, wj, ws, st, h); }));
       }
       ProfScope ps(PK_DOT1);
       TRY(launch_dot1_wo<T>(wj, d.n, V, d.ldv, j + 1, sv, ws, st));
@@ -463,7 +467,10 @@ extern "C" int mpg_solver_begin(mpg_solver* s, void* stream) {
   WsView ws = make_ws(d.ws);
   mpg_state_header* h = hdr_of(d);
   const bool outer64 = d.mode == MPG_MODE_IR || d.prec == MPG_FP64;
-  cudaError_t e = outer64
+  // kernel-time accumulators restart with the solve (the first stamp opens)
+  cudaError_t e = cudaMemsetAsync(h->ktime_ns, 0, sizeof(h->ktime_ns) + sizeof(h->kt_mark), st);
+  if (e) return e;
+  e = outer64
       ? launch_norm2<double>(static_cast<const double*>(d.b), d.n, &h->outer_b_norm, ws, st)
       : launch_norm2<float>(static_cast<const float*>(d.b), d.n, &h->outer_b_norm, ws, st);
   if (e) return e;

@@ -56,6 +56,9 @@ __device__ __forceinline__ void consumers_finalize(const T* part, int nparts, in
 template <typename T>
 struct EpiPlain {
   static constexpr bool kPdl = true;   // the Arnoldi-step SpMV (split K_A)
+  const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
+  int kcat = KC_SPMV;
+  __device__ void mark() const { kt_mark(kt, kcat); }
   T* y;
   __device__ bool skip() const { return false; }
   __device__ void init(EpiShared<T>&, unsigned char*) {}
@@ -73,6 +76,9 @@ struct EpiPlain {
 template <typename T>
 struct EpiResid {
   static constexpr bool kPdl = false;
+  const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
+  int kcat = KC_SPMV;
+  __device__ void mark() const { kt_mark(kt, kcat); }
   const T* b;
   T* r;
   double* out;
@@ -113,6 +119,9 @@ struct EpiResid {
 template <typename T>
 struct EpiDot1 {
   static constexpr bool kPdl = false;
+  const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
+  int kcat = KC_SPMV;
+  __device__ void mark() const { kt_mark(kt, kcat); }
   static constexpr bool kNeedsTiles = true;
   T* w;
   const T* V;
@@ -184,6 +193,9 @@ struct EpiDot1 {
 template <typename T, int KV>
 struct EpiDot1Warp {
   static constexpr bool kPdl = false;
+  const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
+  int kcat = KC_SPMV;
+  __device__ void mark() const { kt_mark(kt, kcat); }
   static constexpr bool kNeedsTiles = true;
   static constexpr int VN = 16 / (int)sizeof(T);
   static constexpr int RB = 32 * VN;
@@ -302,6 +314,9 @@ struct EpiDot1Warp {
 template <typename T>
 struct EpiPoly {
   static constexpr bool kPdl = false;
+  const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
+  int kcat = KC_SPMV;
+  __device__ void mark() const { kt_mark(kt, kcat); }
   int op;
   T a, b;
   const T* src;   // SpMV input (also own-row operand)
@@ -407,6 +422,7 @@ __global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __re
   pdl_wait();
   pdl_trigger();
   if (epi.skip()) return;
+  epi.mark();
   SpSmem<T>& sm = *reinterpret_cast<SpSmem<T>*>(smraw);
   epi.init(sm.es, smraw + sizeof(SpSmem<T>));
   spmv_pipeline(A, x, epi, sm);
@@ -420,6 +436,7 @@ __global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, cons
   pdl_wait();
   pdl_trigger();
   if (epi.skip()) return;
+  epi.mark();
   epi.init(es, smraw);
   stencil_pipeline(S, x, epi, es);
 }
@@ -447,6 +464,7 @@ __global__ void __launch_bounds__(kCsrThreads) k_csr_warp(CsrView<T> A, const T*
   pdl_wait();
   pdl_trigger();
   if (epi.skip()) return;
+  epi.mark();
   epi.init(es, nullptr);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n = A.n;
@@ -607,16 +625,21 @@ static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& e
 }
 
 template <typename T, typename M>
-cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView, cudaStream_t st) {
-  EpiPlain<T> e{y};
+cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView, cudaStream_t st,
+                        const mpg_state_header* kt) {
+  EpiPlain<T> e{};
+  e.y = y;
+  e.kt = kt;
   return launch_matrix(A, x, e, 0, st);
 }
 
 template <typename T, typename M>
 cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
-                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw) {
+                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw,
+                            const mpg_state_header* kt, int kcat) {
   EpiResid<T> e{};
   e.b = b; e.r = r; e.out = norm_out; e.hdr = hdr; e.raw = raw;
+  e.kt = kt; e.kcat = kcat;
   e.part = static_cast<T*>(ws.part);
   e.counter = ws.counter;
   return launch_matrix(A, x, e, 0, st);
@@ -629,6 +652,7 @@ cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long
     constexpr int KV = decltype(tag)::value;
     EpiDot1Warp<T, KV> e{};
     e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
+    e.kt = sv.h;
     e.part = static_cast<T*>(ws.part);
     e.counter = ws.counter;
     return launch_matrix(A, x, e, 0, st);
@@ -646,6 +670,7 @@ cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long
   }
   EpiDot1<T> e{};
   e.w = w; e.V = V; e.ldv = ldv; e.k = k; e.sv = sv;
+  e.kt = sv.h;
   e.part = static_cast<T*>(ws.part);
   e.counter = ws.counter;
   return launch_matrix(A, x, e, (size_t)(k + 8) * sizeof(T), st);
@@ -654,7 +679,7 @@ cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long
 template <typename T, typename M>
 cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, T* t0, T* t1,
                            T* t2, const mpg_state_header* gate, long long n, WsView ws,
-                           cudaStream_t st) {
+                           cudaStream_t st, const mpg_state_header* kt) {
   T* bufs[5] = {const_cast<T*>(x), y, t0, t1, t2};
   EpiPoly<T> e{};
   e.op = op.op;
@@ -665,6 +690,7 @@ cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, 
   e.x2 = bufs[op.x2];
   e.y = y;
   e.gate = gate;
+  e.kt = kt;
   return launch_matrix(A, e.src, e, 0, st);
 }
 
@@ -756,14 +782,16 @@ cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, c
 }
 
 #define INST_M(T, M)                                                                            \
-  template cudaError_t launch_spmv<T, M>(const M&, const T*, T*, WsView, cudaStream_t);         \
+  template cudaError_t launch_spmv<T, M>(const M&, const T*, T*, WsView, cudaStream_t,          \
+                                         const mpg_state_header*);                              \
   template cudaError_t launch_residual<T, M>(const M&, const T*, const T*, T*, double*,         \
-                                             mpg_state_header*, WsView, cudaStream_t, int);    \
+                                             mpg_state_header*, WsView, cudaStream_t, int,     \
+                                             const mpg_state_header*, int);                    \
   template cudaError_t launch_spmv_dot1<T, M>(const M&, const T*, T*, const T*, long long, int, \
                                               StateView<T>, WsView, cudaStream_t);             \
   template cudaError_t launch_poly_op<T, M>(const M&, const mpg_poly_op&, const T*, T*, T*, T*, \
                                             T*, const mpg_state_header*, long long, WsView,    \
-                                            cudaStream_t);
+                                            cudaStream_t, const mpg_state_header*);
 INST_M(float, CsrView<float>)
 INST_M(double, CsrView<double>)
 INST_M(float, StencilView<float>)

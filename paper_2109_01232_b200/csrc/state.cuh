@@ -102,17 +102,19 @@ template <typename T> struct StencilView;
 
 // spmv family (spmv_kernels.cu); M = CsrView<T> or StencilView<T>
 template <typename T, typename M>
-cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView ws, cudaStream_t st);
+cudaError_t launch_spmv(const M& A, const T* x, T* y, WsView ws, cudaStream_t st,
+                        const mpg_state_header* kt = nullptr);
 template <typename T, typename M>
 cudaError_t launch_residual(const M& A, const T* b, const T* x, T* r, double* norm_out,
-                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw = 0);
+                            mpg_state_header* hdr, WsView ws, cudaStream_t st, int raw = 0,
+                            const mpg_state_header* kt = nullptr, int kcat = KC_SPMV);
 template <typename T, typename M>
 cudaError_t launch_spmv_dot1(const M& A, const T* x, T* w, const T* V, long long ldv, int k,
                              StateView<T> sv, WsView ws, cudaStream_t st);
 template <typename T, typename M>
 cudaError_t launch_poly_op(const M& A, const mpg_poly_op& op, const T* x, T* y, T* t0, T* t1,
                            T* t2, const mpg_state_header* gate, long long n, WsView ws,
-                           cudaStream_t st);
+                           cudaStream_t st, const mpg_state_header* kt = nullptr);
 template <typename T>
 cudaError_t launch_stencil_pack(int dims, int nx, long long row0, long long n, const int32_t* rp,
                                 const int32_t* ci, const T* v, T* out, long long ldv, int* bad,

@@ -97,6 +97,11 @@ __global__ void __launch_bounds__(kMegaThreads, 1)
 k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
             T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout) {
   if (gated(sv.h)) return;
+  // kernel-time categories (timing.py): CTA 0 stamps at its own phase ends and
+  // after each grid barrier, so each interval ends when the grid has finished
+  // the phase (B1..B3) or, for the SpMV, when CTA 0 has
+  const bool kt0 = blockIdx.x == 0 && threadIdx.x == 0;
+  if (kt0) kt_stamp(sv.h, KC_SPMV);
   MEGA_STAMP(0)
   constexpr int VN = Vec<T>::n;
   constexpr int RB = 32 * VN;
@@ -179,6 +184,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   __syncthreads();
+  if (kt0) kt_stamp(sv.h, KC_GEMV_T);                    // pass-1 dots up to B1's sums
   MEGA_STAMP(1)
 
   // --------------------------------------------------------- P1b c1 = V^T w
@@ -268,6 +274,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     return;
   }
   const double w0 = (double)sqrt_rn(c1v[k]);
+  if (kt0) kt_stamp(sv.h, KC_GEMV_TN);                   // P2: update + pass-2 dots, to B2
   if (blockIdx.x == 0) {
     if (tid < k) sv.c1[tid] = c1v[tid];
     if (tid == 0) sv.h->w0 = w0;
@@ -379,6 +386,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (lane == 0) c2v[c] = s;
   }
   __syncthreads();
+  if (kt0) kt_stamp(sv.h, KC_GEMV_N);                    // P3: w'' = w' - V c2
   if (blockIdx.x == 0 && tid < k) {
     sv.c2[tid] = c2v[tid];
     sv.Hc(j, tid) = add_rn(add_rn(T(0), c1v[tid]), c2v[tid]);   // h = 0; h += c1; h += c2
@@ -434,6 +442,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     T t = T(0);
     for (int w = 0; w < kMegaWarps; ++w) t += red[w];
     part[(size_t)kColNorm * kMaxParts + blockIdx.x] = t;
+    if (kt0) kt_stamp(sv.h, KC_NORM);                    // B3 + the norm's column sum
   }
   MEGA_STAMP(6)
   grid_barrier(ws.counter, ws.counter + 1);                                       // B3
@@ -444,6 +453,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   }
   __syncthreads();
   const T hs = sqrt_rn(red[0]);
+  if (kt0) kt_stamp(sv.h, KC_OTHER);                     // Givens + V[:, j+1] = w'' / h
   const bool brk = (double)hs <= sv.h->breakdown_tol * w0;   // krylov.py:146
   if (blockIdx.x == 0 && warp == 0) {   // the rotation runs in warp 0 while warps 1.. start P4
     if (lane == 0) {

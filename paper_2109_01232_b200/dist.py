@@ -230,7 +230,7 @@ class DistributedStencilSolver:
         s = self.prec.dtype.itemsize
         red_off = int(lib.mpg_state_offset(self.prec.code, m, 9))
         self.red = self.state.buf[red_off: red_off + s * (m + 8)].view(self.prec.torch_dtype)
-        res_off = C.sizeof(_lib.StateHeader) - 6 * 8          # header reserved[0]
+        res_off = _lib.StateHeader.reserved.offset             # header reserved[0]
         self.reserved0 = self.state.buf[res_off: res_off + 8].view(torch.float64)
         d = _lib.SolverDesc()
         d.mode, d.prec, d.m, d.use_graph = self.mode, self.prec.code, m, 0

@@ -331,11 +331,24 @@ class NativeSolve:
     def begin(self) -> tuple[float, float]:
         _lib.call("mpg_solver_begin", self.handle, stream_handle())
         hdr, _ = self.state.read()
+        self.last_hdr = hdr
         return float(hdr.outer_b_norm), float(hdr.rnorm)
 
     def cycle(self, m_limit: int):
         _lib.call("mpg_solver_cycle", self.handle, int(m_limit), stream_handle())
-        return self.state.read()
+        hdr, imp = self.state.read()
+        self.last_hdr = hdr
+        return hdr, imp
+
+    def bin_kernel_times(self, timer: timing.KernelTimer | None) -> None:
+        """Add the device's per-category kernel time (globaltimer stamps of the
+        cycle kernels, accumulated in the state header since begin()) to
+        ``timer``: the reference's tick/tock binning (timing.py:88-98)."""
+        hdr = getattr(self, "last_hdr", None)
+        if timer is None or hdr is None:
+            return
+        for i, cat in enumerate(timing.KERNEL_CATEGORIES):
+            timer.add(cat, hdr.ktime_ns[i] * 1e-9)
 
     def profile_cycle(self, m_limit: int) -> dict[str, tuple[float, int]]:
         """One eager cycle with per-kernel-class CUDA events: {class: (ms, launches)}."""
@@ -450,6 +463,7 @@ def gmres_restarted(A, b, x0=None, criteria: StopCriteria | None = None, precond
         with timing.active(timer):
             converged, total, loss, stalled_at = _run_restarted(
                 ns, criteria, phase, history, stop_on_stall=stop_on_stall)
+        ns.bin_kernel_times(timer)
     finally:
         ns.close()
     fp32 = precision is FP32
@@ -522,6 +536,7 @@ def gmres_ir(A, b, x0=None, criteria: StopCriteria | None = None, precond_fp32=N
                     if stall_run >= STALL_RESTARTS and stalled_at is None:
                         stalled_at = total
                     prev_rel = explicit_rel
+        ns.bin_kernel_times(timer)
     finally:
         ns.close()
     return SolveReport(
@@ -561,6 +576,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
                     ns32, criteria, "fp32", history, iter_offset=0,
                     limit=min(switch_iter, criteria.max_iters), stop_on_stall=True)
                 xd = padded_copy(convert_vector(ns32.x[:n], FP64), FP64)
+            ns32.bin_kernel_times(timer)
         finally:
             ns32.close()
         if history and history[-1].iteration == iters32:
@@ -572,6 +588,7 @@ def gmres_fd(A, b, x0=None, criteria: StopCriteria | None = None, switch_iter: i
             converged, iters64, loss64, st64 = _run_restarted(
                 ns, criteria, "fp64", history, iter_offset=iters32,
                 limit=max(criteria.max_iters - iters32, 0))
+        ns.bin_kernel_times(timer)
     finally:
         ns.close()
     return SolveReport(

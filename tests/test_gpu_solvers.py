@@ -143,6 +143,35 @@ def test_solver_parity(case, golden_runs):
     assert set(rep.kernel_times) == {"SpMV", "GemvTrans", "Norm", "GemvNoTrans", "Other"}
 
 
+@pytest.mark.parametrize("solver,step", [("fp64", "split"), ("ir", "split"), ("ir", "persistent"),
+                                         ("fp64", "persistent"), ("fd", "auto")])
+def test_kernel_times_partition_total(solver, step):
+    """SolveReport.kernel_times is the reference's partition of total_time
+    (timing.py:40-47): the four kernel bins are filled from the device's
+    globaltimer stamps -- each > 0 for these solves -- and Other is the
+    remainder, so the five sum to total_time."""
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, 40))
+    b = np.ones(A.n_rows)
+    crit = P.StopCriteria(rtol=1e-10, m=50)
+    with P.solvers.step_kernel(step):
+        if solver == "fp64":
+            rep = P.gmres_restarted(A, b, criteria=crit)
+        elif solver == "ir":
+            rep = P.gmres_ir(A, b, criteria=crit)
+        else:
+            rep = P.gmres_fd(A, b, criteria=crit, switch_iter=100)
+    kt = rep.kernel_times
+    assert set(kt) == {"SpMV", "GemvTrans", "Norm", "GemvNoTrans", "Other"}
+    for cat in ("SpMV", "GemvTrans", "Norm", "GemvNoTrans"):
+        assert kt[cat] > 0, kt
+    assert all(v >= 0 for v in kt.values())
+    assert abs(sum(kt.values()) - rep.total_time) <= 1e-9 * max(1.0, rep.total_time) + 1e-12
+    # the binned device time is most of the solve (graph-replayed cycles)
+    assert sum(kt[c] for c in ("SpMV", "GemvTrans", "Norm", "GemvNoTrans")) >= 0.5 * rep.total_time, kt
+    # CGS2 moves ~3 basis sweeps per step against one SpMV: the Gemv bins dominate
+    assert kt["GemvTrans"] + kt["GemvNoTrans"] > kt["SpMV"], kt
+
+
 def test_golden_235_and_determinism():
     Ao = O.stencil_csr("laplace2d", 50)
     A = dev(Ao)
