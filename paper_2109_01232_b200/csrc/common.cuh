@@ -202,6 +202,21 @@ __device__ __forceinline__ void cta_rows(long long n, long long& r0, long long& 
 }
 
 // ---------------------------------------------------------------------------
+// Per-thread asynchronous global -> shared copies (cp.async, SASS LDGSTS):
+// no register staging, so a warp keeps a whole chunk's loads in flight.
+template <int B>
+__device__ __forceinline__ void cp_async_ca(void* smem, const void* g) {
+  static_assert(B == 4 || B == 8 || B == 16, "cp.async sizes");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(g), "n"(B)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---------------------------------------------------------------------------
 // mbarrier + TMA bulk copy (cp.async.bulk, SASS UBLKCP) helpers
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -229,6 +244,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // 1-D bulk global->shared copy; dst/src 16-byte aligned, bytes % 16 == 0.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -305,6 +323,20 @@ __device__ __forceinline__ T pairwise(const Get& get, int i0, int n) {
   }
   if (n <= 128) return pairwise_block<T>(get, i0, n);
   return pairwise_split<T>(get, i0, n);
+}
+
+// row_reduce over precomputed products p[0..len), len <= N <= 8: the same
+// association (p0 + sequential sum of p1.. from -0.0, numpy's n < 8 path)
+template <typename T, int N>
+__device__ __forceinline__ T row_sum_short(const T (&p)[N], int len) {
+  static_assert(N <= 8, "pairwise's sequential branch covers fewer than 8 terms after p0");
+  if (len <= 0) return T(0);
+  if (len == 1) return p[0];
+  T r = T(-0.0);
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    if (i < len) r = add_rn(r, p[i]);
+  return add_rn(p[0], r);
 }
 
 template <typename T, typename Get>

@@ -445,21 +445,139 @@ __global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, cons
 // CSR SpMV, warp-chunk design (the default for epilogues without a per-tile
 // hook): each warp owns chunks of 32 consecutive rows dealt round-robin over
 // every warp of the grid.  The chunk's nonzeros are one contiguous range of
-// col_idx / values, so the warp stages it into its own shared-memory slice
-// with coalesced loads (all independent, issued back to back), then lane l
-// reduces row l from shared memory in the reference's add.reduceat order,
-// gathering x through the read-only path.  A chunk with more than kCsrCap
-// nonzeros (long rows) is reduced straight from global memory.  No CTA-wide
-// barrier, no producer warp: ~48 warps per SM stream independently (the
-// TMA-ring kernel ran at one CTA of 9 warps per SM in fp64).
+// col_idx / values, which the warp copies into its own shared-memory slice
+// with per-lane cp.async (LDGSTS, no register staging); lane l then reduces
+// row l from shared memory in the reference's add.reduceat order, gathering
+// x through the read-only path -- rows of <= 8 entries issue all their x
+// gathers at once.  Software pipeline, per warp: while chunk c is reduced,
+// chunk c+1's nonzeros are in flight into the other slice and chunk c+2's
+// row_ptr entries are in registers, so the dependent chain row_ptr -> values
+// -> x costs one exposed latency per chunk instead of three.  A chunk with
+// more than csr_cap() nonzeros (long rows) is reduced straight from global
+// memory.  No CTA-wide barrier, no producer warp.
 constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
-constexpr int kCsrCap = 384;   // staged nonzeros per warp chunk (avg <= 12 per row)
+#ifndef MPG_CSR_CAP
+#define MPG_CSR_CAP 256
+#endif
+#ifndef MPG_CSR_MINB
+#define MPG_CSR_MINB 4
+#endif
+#ifndef MPG_CSR_SHORT
+#define MPG_CSR_SHORT 1   // A/B: 0 = one dependent gather per product
+#endif
+// rows per lane: a warp chunk is 32 * RPL consecutive rows (lane l owns rows
+// l, l + 32, ...), so the per-chunk bookkeeping (row_ptr shuffles, staging
+// loop, loop control) is amortised over RPL rows and every lane has RPL rows'
+// x gathers in flight
+#ifndef MPG_CSR_RPL32
+#define MPG_CSR_RPL32 1
+#endif
+#ifndef MPG_CSR_RPL64
+#define MPG_CSR_RPL64 1
+#endif
+template <typename T>
+constexpr int csr_rpl() { return sizeof(T) == 8 ? MPG_CSR_RPL64 : MPG_CSR_RPL32; }
+constexpr int kCsrShort = 8;           // rows up to this length gather all of x before summing
+// slices per warp = pipeline depth (chunks in flight + the one being reduced).
+// 2 (measured: 3 slices in fp32 / fp64 ran 2-3 % / 25 % slower -- the extra
+// slice costs occupancy and the chain is bound by the x gathers, not staging;
+// issuing the next chunk's x gathers a whole iteration ahead was 4 % slower)
+constexpr int kCsrBufs = 2;
+template <typename T>
+constexpr int csr_cap() { return MPG_CSR_CAP * csr_rpl<T>(); }   // staged nonzeros per chunk and slice
+// staging engine: per-warp TMA bulk copies (one cp.async.bulk per array and
+// chunk, completion on a per-slice mbarrier) or per-lane cp.async (LDGSTS)
+#ifndef MPG_CSR_BULK
+#define MPG_CSR_BULK 1
+#endif
+// slice length: the bulk copies move the 16-byte-aligned superset of the
+// chunk's range (at most 3 extra elements at each end)
+template <typename T>
+constexpr int csr_slice() { return csr_cap<T>() + (MPG_CSR_BULK ? 8 : 0); }
+template <typename T>
+constexpr size_t csr_smem_bytes() { return (size_t)kCsrBufs * kCsrWarps * csr_slice<T>() * (sizeof(T) + 4); }
 
+template <int R>
+struct CsrChunk {
+  int lo[R], hi[R];   // this lane's row ranges
+  int s, e;           // the chunk's nonzero range (warp-uniform)
+};
+// row_ptr entries of chunk c, as loaded (rows past n clamp to row_ptr[n]: an
+// empty chunk).  csr_chunk() shuffles them into the lane's row ranges only
+// when the chunk is staged, one iteration later, so the loads are a real
+// prefetch.
+template <int R>
+struct CsrRaw {
+  int q[R], qe;
+};
+template <int R>
+__device__ __forceinline__ CsrRaw<R> csr_load(const int32_t* __restrict__ rp, long long n, long long c,
+                                              int lane) {
+  const long long r0 = c * 32 * R;
+  CsrRaw<R> w;
+#pragma unroll
+  for (int j = 0; j < R; ++j) w.q[j] = __ldg(rp + min(r0 + 32 * j + lane, n));
+  w.qe = __ldg(rp + min(r0 + 32 * R, n));
+  return w;
+}
+template <int R>
+__device__ __forceinline__ CsrChunk<R> csr_chunk(const CsrRaw<R>& w, int lane) {
+  CsrChunk<R> k;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int nxt = __shfl_down_sync(0xffffffffu, w.q[j], 1);
+    const int first_next = j + 1 < R ? __shfl_sync(0xffffffffu, w.q[j + 1 < R ? j + 1 : j], 0) : w.qe;
+    k.lo[j] = w.q[j];
+    k.hi[j] = lane < 31 ? nxt : first_next;
+  }
+  k.s = __shfl_sync(0xffffffffu, w.q[0], 0);
+  k.e = w.qe;
+  return k;
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void csr_stage(const CsrView<T>& A, const CsrChunk<R>& k, T* v_s, int32_t* ci_s,
+                                          int lane, uint64_t* bar) {
+  constexpr int cap = csr_cap<T>();
+  const int cnt = k.e - k.s;
+  if constexpr (MPG_CSR_BULK) {
+    // lane 0: two bulk copies of the aligned supersets (the C ABI guarantees
+    // 16-byte-aligned arrays with 16 readable bytes past their end)
+    if (lane == 0) {
+      if (cnt > 0 && cnt <= cap) {
+        constexpr int VE = 16 / (int)sizeof(T);
+        const int s4 = k.s & ~3, e4 = (k.e + 3) & ~3;
+        const int sv = k.s & ~(VE - 1), ev = (k.e + VE - 1) & ~(VE - 1);
+        const uint32_t bc = (uint32_t)(e4 - s4) * 4u, bv = (uint32_t)(ev - sv) * (uint32_t)sizeof(T);
+        fence_proxy_async();   // this warp's generic reads of the slice precede the async writes
+        mbar_expect_tx(bar, bc + bv);
+        bulk_g2s(ci_s, A.ci + s4, bc, bar);
+        bulk_g2s(v_s, A.v + sv, bv, bar);
+      } else {
+        mbar_arrive(bar);      // nothing to stage: complete the phase
+      }
+    }
+  } else {
+    if (cnt <= cap) {
+#pragma unroll
+      for (int it = 0; it < cap / 32; ++it) {
+        const int i = lane + 32 * it;
+        if (i < cnt) {
+          cp_async_ca<4>(ci_s + i, A.ci + k.s + i);
+          cp_async_ca<(int)sizeof(T)>(v_s + i, A.v + k.s + i);
+        }
+      }
+    }
+    cp_async_commit();   // one group per chunk, empty for long-row or past-the-end chunks
+  }
+}
 
 template <typename T, typename E>
-__global__ void __launch_bounds__(kCsrThreads) k_csr_warp(CsrView<T> A, const T* __restrict__ x, E epi) {
-  extern __shared__ __align__(16) unsigned char csr_smem[];   // [warps][cap] T, then [warps][cap] int32
+__global__ void __launch_bounds__(kCsrThreads, MPG_CSR_MINB) k_csr_warp(CsrView<T> A, const T* __restrict__ x, E epi) {
+  constexpr int R = csr_rpl<T>();
+  constexpr int cap = csr_cap<T>();
+  extern __shared__ __align__(16) unsigned char csr_smem[];   // [bufs][warps][cap] T, then int32
   __shared__ EpiShared<T> es;
   pdl_wait();
   pdl_trigger();
@@ -468,42 +586,84 @@ __global__ void __launch_bounds__(kCsrThreads) k_csr_warp(CsrView<T> A, const T*
   epi.init(es, nullptr);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long n = A.n;
-  const long long nchunks = (n + 31) / 32;
+  const long long nchunks = (n + 32 * R - 1) / (32 * R);
   const long long gw = (long long)blockIdx.x * kCsrWarps + warp;
   const long long nw = (long long)gridDim.x * kCsrWarps;
-  T* v_s = reinterpret_cast<T*>(csr_smem) + (size_t)warp * kCsrCap;
-  int32_t* ci_s = reinterpret_cast<int32_t*>(csr_smem + sizeof(T) * kCsrWarps * kCsrCap) + (size_t)warp * kCsrCap;
-  for (long long c = gw; c < nchunks; c += nw) {
-    const long long r = c * 32 + lane;
-    const bool in = r < n;
-    const int lo = in ? __ldg(A.rp + r) : 0;
-    const int hi = in ? __ldg(A.rp + r + 1) : 0;
-    const long long rlast = min(c * 32 + 31, n - 1);
-    const int s = __shfl_sync(0xffffffffu, lo, 0);
-    const int e = __ldg(A.rp + rlast + 1);
-    const int cnt = e - s;
-    T y = T(0);
-    if (cnt <= kCsrCap) {
-      __syncwarp();   // the previous chunk's readers are done with the slice
-#pragma unroll 4
-      for (int i = lane; i < cnt; i += 32) {
-        ci_s[i] = __ldcs(A.ci + s + i);
-        v_s[i] = __ldcs(A.v + s + i);
+  constexpr int SL = csr_slice<T>();
+  T* vbase = reinterpret_cast<T*>(csr_smem);
+  int32_t* cbase = reinterpret_cast<int32_t*>(csr_smem + sizeof(T) * kCsrBufs * kCsrWarps * SL);
+  auto vslice = [&](int b) { return vbase + ((size_t)b * kCsrWarps + warp) * SL; };
+  auto cslice = [&](int b) { return cbase + ((size_t)b * kCsrWarps + warp) * SL; };
+  __shared__ uint64_t bars[kCsrWarps][kCsrBufs];
+  if (MPG_CSR_BULK && lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  // where element i of the chunk's range landed in a slice
+  constexpr int VE = MPG_CSR_BULK ? 16 / (int)sizeof(T) : 1;
+  constexpr int CE = MPG_CSR_BULK ? 4 : 1;
+  if (gw < nchunks) {
+    // cur: chunk c (in flight); nxt: chunk c + nw (staged at the top of the
+    // iteration); raw: row_ptr loads of chunk c + 2 nw
+    CsrChunk<R> cur = csr_chunk<R>(csr_load<R>(A.rp, n, gw, lane), lane);
+    csr_stage<T, R>(A, cur, vslice(0), cslice(0), lane, &bars[warp][0]);
+    CsrRaw<R> raw = csr_load<R>(A.rp, n, gw + nw, lane);
+    int buf = 0;
+    uint32_t ph = 0;   // bit b: parity of slice b's next completion
+    for (long long c = gw; c < nchunks; c += nw) {
+      __syncwarp();   // every lane is done reading the other slice (chunk c - nw)
+      const CsrChunk<R> nxt = csr_chunk<R>(raw, lane);
+      csr_stage<T, R>(A, nxt, vslice(buf ^ 1), cslice(buf ^ 1), lane, &bars[warp][buf ^ 1]);
+      raw = csr_load<R>(A.rp, n, c + 2 * nw, lane);
+      if constexpr (MPG_CSR_BULK) {
+        mbar_wait(&bars[warp][buf], (ph >> buf) & 1u);   // chunk c's copies landed
+        ph ^= 1u << buf;
+      } else {
+        cp_async_wait<1>();   // chunk c's group; chunk c + nw's may still fly
+        __syncwarp();
       }
-      __syncwarp();
-      if (in) {
-        const int32_t* cs = ci_s + (lo - s);
-        const T* vs = v_s + (lo - s);
-        auto get = [&](int i) -> T { return mul_rn(vs[i], __ldg(x + cs[i])); };
-        y = row_reduce<T>(get, hi - lo);
+      const bool staged = cur.e - cur.s <= cap;
+      const int cofs = cur.s & ~(CE - 1), vofs = cur.s & ~(VE - 1);
+      T y[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int len = cur.hi[j] - cur.lo[j];
+        if (staged && MPG_CSR_SHORT && len <= kCsrShort) {
+          // all of the row's x gathers in flight at once (predicated), then the
+          // reference's order p0 + (((p1 + p2) + p3) ...) (row_reduce, len <= 8)
+          const int32_t* cs = cslice(buf) + (cur.lo[j] - cofs);
+          const T* vs = vslice(buf) + (cur.lo[j] - vofs);
+          T p[kCsrShort];
+#pragma unroll
+          for (int i = 0; i < kCsrShort; ++i) p[i] = i < len ? mul_rn(vs[i], __ldg(x + cs[i])) : T(0);
+          y[j] = row_sum_short<T, kCsrShort>(p, len);
+        } else if (staged) {
+          const int32_t* cs = cslice(buf) + (cur.lo[j] - cofs);
+          const T* vs = vslice(buf) + (cur.lo[j] - vofs);
+          auto get = [&](int i) -> T { return mul_rn(vs[i], __ldg(x + cs[i])); };
+          y[j] = row_reduce<T>(get, len);
+        } else {
+          const int32_t* cg = A.ci + cur.lo[j];
+          const T* vg = A.v + cur.lo[j];
+          auto get = [&](int i) -> T { return mul_rn(__ldg(vg + i), __ldg(x + __ldg(cg + i))); };
+          y[j] = row_reduce<T>(get, len);
+        }
       }
-    } else if (in) {
-      const int32_t* cg = A.ci + lo;
-      const T* vg = A.v + lo;
-      auto get = [&](int i) -> T { return mul_rn(__ldg(vg + i), __ldg(x + __ldg(cg + i))); };
-      y = row_reduce<T>(get, hi - lo);
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const long long r = c * 32 * R + 32 * j + lane;
+        if (r < n) epi.on_row(r, y[j]);
+      }
+      cur = nxt;
+      buf ^= 1;
     }
-    if (in) epi.on_row(r, y);
+    if constexpr (MPG_CSR_BULK) {
+      mbar_wait(&bars[warp][buf], (ph >> buf) & 1u);   // the last (empty) stage before exit
+    } else {
+      cp_async_wait<0>();
+    }
   }
   epi.on_end();
 }
@@ -568,7 +728,7 @@ static cudaError_t launch_matrix(const CsrView<T>& A, const T* x, const E& epi, 
     if (csr_warp_enabled()) {
       static std::once_flag once_w;
       static int occ_w = 1;
-      constexpr size_t dsm = (size_t)kCsrWarps * kCsrCap * (sizeof(T) + 4);
+      constexpr size_t dsm = csr_smem_bytes<T>();
       std::call_once(once_w, [&] {
         cudaFuncSetAttribute(k_csr_warp<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_csr_warp<T, E>, kCsrThreads, dsm);
