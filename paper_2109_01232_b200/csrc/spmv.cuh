@@ -343,19 +343,13 @@ __device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)
 // loaded (absent neighbours read padding / the sentinel value) and add.reduceat's
 // order p0 + (((p1 + p2) + p3) ...) over the present slots is applied with
 // selects: bit-exact.
+// The x operands of one row group (stencil_group's loads, issued together):
+// px[s][e] = x[r0 + e + off[s]].
 template <typename T, int S>
-__device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
-                                              long long r0, const long long (&off)[S],
-                                              const int (&mis)[S], const StencilConst<T, S>& K,
-                                              T (&y)[Vec<T>::n]) {
+__device__ __forceinline__ void stencil_xload(const T* __restrict__ x, long long r0, const long long (&off)[S],
+                                              const int (&mis)[S], T (&px)[S][Vec<T>::n]) {
   constexpr int VN = Vec<T>::n;
   constexpr int C = S / 2;   // centre slot; C - 1 / C + 1 are the x -+ 1 neighbours
-  const size_t ld = (size_t)SV.ldv;
-  T pv[S][VN], px[S][VN];
-  if (!K.on) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
-  }
   vload(x + r0, px[C]);
   const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
 #pragma unroll
@@ -367,7 +361,54 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
 #pragma unroll
   for (int e = 0; e < VN - 1; ++e) px[C + 1][e] = px[C][e + 1];
   px[C + 1][VN - 1] = xp;
-  if (K.on) {   // coefficients from registers, presence from the grid coordinates
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void stencil_const_rows(const StencilView<T>& SV, long long r0,
+                                                   const StencilConst<T, S>& K, const T (&px)[S][Vec<T>::n],
+                                                   T (&y)[Vec<T>::n]);
+
+template <typename T, int S>
+__device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
+                                              long long r0, const long long (&off)[S],
+                                              const int (&mis)[S], const StencilConst<T, S>& K,
+                                              T (&y)[Vec<T>::n]) {
+  constexpr int VN = Vec<T>::n;
+  const size_t ld = (size_t)SV.ldv;
+  T pv[S][VN], px[S][VN];
+  if (!K.on) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
+  }
+  stencil_xload<T, S>(x, r0, off, mis, px);
+  if (K.on) {
+    stencil_const_rows<T, S>(SV, r0, K, px, y);
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < VN; ++e) {
+    bool have = false;
+    T p0 = T(0), rest = T(-0.0);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const T p = mul_rn(pv[s][e], px[s][e]);
+      const bool pr = present(pv[s][e]);
+      const T nrest = add_rn(rest, p);
+      rest = (pr && have) ? nrest : rest;
+      p0 = (pr && !have) ? p : p0;
+      have = have || pr;
+    }
+    y[e] = add_rn(p0, rest);
+  }
+}
+
+// Constant-coefficient rows of one group from its loaded x operands.
+template <typename T, int S>
+__device__ __forceinline__ void stencil_const_rows(const StencilView<T>& SV, long long r0,
+                                                   const StencilConst<T, S>& K, const T (&px)[S][Vec<T>::n],
+                                                   T (&y)[Vec<T>::n]) {
+  constexpr int VN = Vec<T>::n;
+  {   // coefficients from registers, presence from the grid coordinates
     const unsigned nx = (unsigned)SV.nx;
     const unsigned ur0 = (unsigned)(r0 + SV.row0);
     const unsigned q0 = div_nx(ur0, K.mg);
@@ -417,22 +458,6 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
       }
       y[e] = add_rn(p0, rest);
     }
-    return;
-  }
-#pragma unroll
-  for (int e = 0; e < VN; ++e) {
-    bool have = false;
-    T p0 = T(0), rest = T(-0.0);
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const T p = mul_rn(pv[s][e], px[s][e]);
-      const bool pr = present(pv[s][e]);
-      const T nrest = add_rn(rest, p);
-      rest = (pr && have) ? nrest : rest;
-      p0 = (pr && !have) ? p : p0;
-      have = have || pr;
-    }
-    y[e] = add_rn(p0, rest);
   }
 }
 

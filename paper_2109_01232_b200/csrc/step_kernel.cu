@@ -164,23 +164,30 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
   K.on = KONST;
   T ss = T(0);
   int bad = 0;
-  for (int L = tid; L < nb * 32; L += kMegaThreads) {
-    const int t = L >> 5, l = L & 31;
-    const long long r0 = bstart(t) + (long long)l * VN;
-    T y[VN];
-    if (r0 < n) {
-      stencil_group<T, S>(SV, x, r0, off, mis, K, y);
+  // one row group's SpMV result -> w (smem or global), ||w||^2, finite flag
+  auto p1_emit = [&](int L, long long r0, T (&y)[VN]) {
 #pragma unroll
-      for (int e = 0; e < VN; ++e) y[e] = r0 + e < n ? y[e] : T(0);
-    } else {
-#pragma unroll
-      for (int e = 0; e < VN; ++e) y[e] = T(0);
-    }
-    if (CACHE || r0 < n) vstore(wptr(t) + l * VN, y);   // global w ends at ldv
+    for (int e = 0; e < VN; ++e) y[e] = r0 + e < n ? y[e] : T(0);
+    if (CACHE || r0 < n) vstore(wptr(L >> 5) + (L & 31) * VN, y);   // global w ends at ldv
 #pragma unroll
     for (int e = 0; e < VN; ++e) {
       ss = fma_rn(y[e], y[e], ss);
       bad |= !isfinite(y[e]);
+    }
+  };
+  auto p1_r0 = [&](int L) { return bstart(L >> 5) + (long long)(L & 31) * VN; };
+  // (two row groups' x loads in flight per thread measured slower: P1 13.4 ->
+  // 18.4 us at k = 27, cfg2 fp32 -- the phase is not bound by loads in flight)
+  {
+    for (int L = tid; L < nb * 32; L += kMegaThreads) {
+      const long long r0 = p1_r0(L);
+      T y[VN];
+      if (r0 < n) stencil_group<T, S>(SV, x, r0, off, mis, K, y);
+      else {
+#pragma unroll
+        for (int e = 0; e < VN; ++e) y[e] = T(0);
+      }
+      p1_emit(L, r0, y);
     }
   }
   __syncthreads();

@@ -8,7 +8,13 @@ import paper_2109_01232_b200 as P
 from paper_2109_01232_b200 import _lib
 A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, int(sys.argv[1]) if len(sys.argv) > 1 else 150))
 b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
-P.gmres_ir(A, b, criteria=P.StopCriteria(rtol=1e-10, m=50, max_iters=50), use_graph=False)
+solver = sys.argv[2] if len(sys.argv) > 2 else "ir"
+crit = P.StopCriteria(rtol=1e-10, m=50, max_iters=50)
+if solver == "ir":
+    P.gmres_ir(A, b, criteria=crit, use_graph=False)
+else:   # fp64 GMRES: force the persistent step (MPG_MEGA=1 or step_kernel("persistent"))
+    with P.solvers.step_kernel("persistent"):
+        P.gmres_restarted(A, b, criteria=crit, use_graph=False)
 torch.cuda.synchronize()
 buf = (C.c_ulonglong * (296 * 10))()
 _lib.load().mpg_debug_mega_times(buf)
