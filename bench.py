@@ -251,6 +251,10 @@ def native_arm(args, rank: int, world: int):
     dom = max((k for k in model if k in prof), key=lambda k: prof[k][0])
     dom_gbs = model[dom] / (prof[dom][0] / 1e3) / 1e9
 
+    # BASELINE configs[4] (64M rows) on this GPU: two restart cycles (north_star's
+    # per-kernel GB/s at the 400^3 size); skipped with --no-cfg5
+    cfg5 = None if args.no_cfg5 else cfg5_segment_single()
+
     # end to end through the public API with HOST inputs (numpy CSR + b)
     rp, ci, v = A.host_arrays()
 
@@ -313,6 +317,7 @@ def native_arm(args, rank: int, world: int):
                      **_traffic(dom)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "cfg5_segment": cfg5,
         "e2e": {"value": round(e2e_s, 5), "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "iters": rep_h.total_iters,
                 "step_times_s": [round(t, 5) for t in e2e_times],
@@ -320,6 +325,138 @@ def native_arm(args, rank: int, world: int):
                         "wall clock per call, mean of the timed steps after one untimed call"},
     }
     return out
+
+
+
+def _max_over_ranks_profile(prof: dict) -> dict:
+    """Per-class device ms of one rank's profiled cycle -> max over ranks (the
+    slowest rank sets the pace), with this rank's bytes (ranks hold equal
+    plane counts up to one plane) and the communication share."""
+    import torch
+    keys = sorted(prof)
+    t = torch.tensor([prof[k]["ms"] for k in keys], dtype=torch.float64, device="cuda")
+    if torch.distributed.is_initialized():
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    out = {}
+    for i, k in enumerate(keys):
+        d = dict(prof[k])
+        d["ms"] = round(float(t[i]), 4)
+        if d.get("bytes") and d["ms"] > 0:
+            d["GBps"] = round(d["bytes"] / (d["ms"] / 1e3) / 1e9, 1)
+        out[k] = d
+    total = sum(d["ms"] for d in out.values())
+    comm = sum(out[k]["ms"] for k in ("allreduce", "halo", "post") if k in out)
+    out["_summary"] = {"cycle_ms": round(total, 4), "comm_ms": round(comm, 4),
+                       "comm_share": round(comm / total, 4) if total else None,
+                       "note": "per rank, max over ranks; comm = allreduce + halo exchange + post kernels"}
+    return out
+
+
+def _dist_roofline(prof: dict) -> dict | None:
+    """Roofline of the dominant phase kernel class of a distributed cycle
+    (algorithmic bytes of this rank's rows / device time, max over ranks)."""
+    cls = [k for k in ("spmv_dot", "update_dot", "update_norm", "scale") if k in prof and prof[k].get("GBps")]
+    if not cls:
+        return None
+    dom = max(cls, key=lambda k: prof[k]["ms"])
+    peak, kind = _peaks()
+    a = prof[dom]["GBps"]
+    return {"bound": "hbm", "kernel": dom, "achieved": a, "peak": peak, "peak_kind": kind, "unit": "GB/s",
+            "frac": round(a / peak, 4), "algorithmic_bytes_per_cycle": prof[dom]["bytes"],
+            "launches_per_cycle": prof[dom]["launches"], "traffic": None,
+            "note": "per rank; ncu is not run on multi-rank commands (B200_PROFILING.md)"}
+
+
+CFG5_NX = 400          # BASELINE configs[4]: Laplace3D 400^3, 64M rows
+CFG5_ITERS = 100       # two restart cycles (SURVEY.md §8d: time 1-2 cycles, report s/iteration)
+
+
+def cfg5_segment_single() -> dict:
+    """BASELINE configs[4] on one GPU: GMRES-IR and fp64 GMRES(50) for a fixed
+    two restart cycles of Laplace3D 400^3 (64M rows; the full solve needs
+    ~15k iterations), s/iteration, the per-kernel-class GB/s of one profiled
+    IR cycle and the explicit residual reached."""
+    import torch
+    import paper_2109_01232_b200 as P
+    from paper_2109_01232_b200 import _lib
+    from paper_2109_01232_b200.core import FP32, FP64, convert_matrix, padded_copy, dvec
+    from paper_2109_01232_b200.solvers import NativeSolve, StopCriteria, gmres_ir
+    A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, CFG5_NX))
+    n, nnz = A.n_rows, A.nnz
+    b = torch.ones(n, dtype=torch.float64, device="cuda")
+    crit = StopCriteria(rtol=RTOL, m=M, max_iters=CFG5_ITERS)
+    out = {"workload": f"laplace3d:{CFG5_NX} (BASELINE configs[4]), GMRES(50), {CFG5_ITERS} iterations",
+           "n": n, "nnz": nnz}
+    for name, f in (("ir", lambda: gmres_ir(A, b, criteria=crit)),
+                    ("fp64", lambda: P.gmres_restarted(A, b, criteria=crit))):
+        f()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = f()
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        out[name] = {"s": round(t, 4), "iters": rep.total_iters, "s_per_iter": round(t / rep.total_iters, 6),
+                     "explicit_rel_residual": rep.residual_history[-1].explicit}
+    out["speedup_ir_vs_fp64"] = round(out["fp64"]["s"] / out["ir"]["s"], 3)
+    A32 = convert_matrix(A, FP32)
+    ns = NativeSolve(_lib.MODE_IR, FP32, A32, A, padded_copy(b, FP64), dvec(n, FP64), M, RTOL)
+    ns.begin()
+    ns.cycle(M)
+    prof = ns.profile_cycle(M)
+    used = ns.storage
+    ns.close()
+    model = cycle_bytes(n, nnz, M, 4, used)
+    if prof.get("dot1", (0.0, 0))[1] > 0:
+        model = split_cycle_bytes(model, n, nnz, M, 4, used)
+    kern = {}
+    for k, (ms, cnt) in prof.items():
+        if cnt:
+            kern[k] = {"ms_per_cycle": round(ms, 4), "launches": cnt}
+            if k in model and ms > 0:
+                kern[k]["GBps"] = round(model[k] / (ms / 1e3) / 1e9, 1)
+    out["profile_cycle"] = {"storage": used, "kernels": kern}
+    del A, A32, b
+    torch.cuda.empty_cache()
+    return out
+
+
+def cfg5_segment_dist(world: int, rank: int, coll, peer: bool) -> dict:
+    """BASELINE configs[4] row-partitioned over the ranks: GMRES-IR for a fixed
+    two restart cycles of Laplace3D 400^3, s/iteration (max over ranks), the
+    profiled cycle's per-phase GB/s and communication share."""
+    import torch
+    import paper_2109_01232_b200 as P
+    from paper_2109_01232_b200.dist import DistributedStencilSolver, RowPartition, _dist_solve
+    from paper_2109_01232_b200.solvers import StopCriteria
+    spec = P.StencilSpec(P.StencilKind.LAPLACE3D, CFG5_NX)
+    part = RowPartition.for_stencil(3, CFG5_NX, world, rank)
+    crit = StopCriteria(rtol=RTOL, m=M, max_iters=CFG5_ITERS)
+    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer)
+    try:
+        solver.x_buf.zero_()
+        _dist_solve(solver, crit, True, None)                 # warm (graphs captured)
+        solver.x_buf.zero_()
+        torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = _dist_solve(solver, crit, True, None)
+        e1.record()
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        solver.x_buf.zero_()
+        solver.begin()
+        prof = _max_over_ranks_profile(solver.profile_cycle(M))
+    finally:
+        solver.close()
+    ts = float(t.item())
+    return {"workload": f"laplace3d:{CFG5_NX} (BASELINE configs[4]) row-partitioned over {world} ranks, "
+                        f"GMRES-IR GMRES(50), {CFG5_ITERS} iterations",
+            "n": CFG5_NX ** 3, "n_local": part.n_local, "s": round(ts, 4), "iters": rep.total_iters,
+            "s_per_iter": round(ts / max(rep.total_iters, 1), 6),
+            "explicit_rel_residual": rep.residual_history[-1].explicit,
+            "profile_cycle": prof, "roofline": _dist_roofline(prof)}
 
 
 def _traffic(cls: str) -> dict:
@@ -392,6 +529,11 @@ def dist_arm(args, rank: int, world: int):
     t = torch.tensor([e0.elapsed_time(e1) / 1e3], device="cuda")
     torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     solve_s = float(t.item()) / args.steps
+    # one eager profiled cycle: per-phase device time, GB/s, communication share
+    solver.x_buf.zero_()
+    solver.begin()
+    prof = _max_over_ranks_profile(solver.profile_cycle(M))
+    cfg5 = cfg5_segment_dist(world, rank, coll, peer)
     # e2e: public distributed API with a host right-hand side slice, x downloaded
     b_host = np.ones(part.n_local)
     torch.distributed.barrier()
@@ -420,7 +562,9 @@ def dist_arm(args, rank: int, world: int):
                    "l2": "working set >> L2 per rank at N<=8; no flush needed"},
         "iters": rep.total_iters, "iters_reference": REFERENCE_IR_ITERS,
         "storage": "stencil", "gpu_launches": launches, "clocks": clk.summary(),
-        "roofline": None,
+        "profile_cycle": prof,
+        "roofline": _dist_roofline(prof),
+        "cfg5_segment": cfg5,
         "e2e": {"value": round(float(e2e.item()), 5), "unit": "s",
                 "h2d_bytes_per_step": int(b_host.nbytes) * world, "d2h_bytes_per_step": int(x_host.nbytes) * world,
                 "iters": rep_h.total_iters},
@@ -527,6 +671,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the 400^3 (configs[4]) segment")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

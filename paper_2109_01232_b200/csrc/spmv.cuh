@@ -403,61 +403,88 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
 }
 
 // Constant-coefficient rows of one group from its loaded x operands.
+// Presence comes from the grid coordinates of the group's first row (two exact
+// multiply-shift divisions); the other rows' coordinates are stepped from it.
+//  - interior groups (every slot present in all VN rows): p0 + (((p1 + p2) + p3) ...)
+//  - x-boundary groups inside the y/z interior (first / last group of an x-line,
+//    the common boundary case: ~2 groups per line): only the x-1 / x+1 slots can
+//    be absent, both inside the "rest" chain, so they are skipped with one
+//    select each and p0 stays the z-1 (2-D: y-1) product
+//  - y/z-boundary planes and line-straddling groups: per-slot presence
+// Every path sums exactly the present slots in add.reduceat's order: bit-exact.
 template <typename T, int S>
 __device__ __forceinline__ void stencil_const_rows(const StencilView<T>& SV, long long r0,
                                                    const StencilConst<T, S>& K, const T (&px)[S][Vec<T>::n],
                                                    T (&y)[Vec<T>::n]) {
   constexpr int VN = Vec<T>::n;
-  {   // coefficients from registers, presence from the grid coordinates
-    const unsigned nx = (unsigned)SV.nx;
-    const unsigned ur0 = (unsigned)(r0 + SV.row0);
-    const unsigned q0 = div_nx(ur0, K.mg);
-    const unsigned ix0 = ur0 - q0 * nx;
-    bool inner;
+  constexpr int XM = S / 2 - 1, XP = S / 2 + 1;   // the x-1 / x+1 slots
+  const unsigned nx = (unsigned)SV.nx;
+  const unsigned ur0 = (unsigned)(r0 + SV.row0);
+  const unsigned q0 = div_nx(ur0, K.mg);
+  const unsigned ix0 = ur0 - q0 * nx;
+  unsigned iy0, iz0;
+  bool yz;   // every row of the group has all its y / z neighbours
+  if constexpr (S == 7) {
+    iz0 = div_nx(q0, K.mg);
+    iy0 = q0 - iz0 * nx;
+    yz = iy0 >= 1 && iy0 + 2 <= nx && iz0 >= 1 && iz0 + 2 <= nx;
+  } else {
+    iz0 = 0;
+    iy0 = q0;
+    yz = q0 >= 1 && q0 + 2 <= nx;
+  }
+  if (yz && ix0 >= 1 && ix0 + VN + 1 <= nx) {   // interior
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      T rest = mul_rn(K.kc[1], px[1][e]);
+#pragma unroll
+      for (int s = 2; s < S; ++s) rest = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
+      y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
+    }
+    return;
+  }
+  if (yz && ix0 + VN <= nx) {   // x-boundary group within one x-line
+#pragma unroll
+    for (int e = 0; e < VN; ++e) {
+      const unsigned ix = ix0 + (unsigned)e;
+      T rest = T(-0.0);   // (2-D: the x-1 slot is p1 itself)
+#pragma unroll
+      for (int s = 1; s < S; ++s) {
+        const T nr = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
+        rest = s == XM ? (ix > 0 ? nr : rest) : (s == XP ? (ix + 1 < nx ? nr : rest) : nr);
+      }
+      y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
+    }
+    return;
+  }
+  unsigned ix = ix0, iy = iy0, iz = iz0;
+#pragma unroll
+  for (int e = 0; e < VN; ++e) {   // per-row presence; coordinates stepped, not divided
+    if (e > 0 && ++ix == nx) {
+      ix = 0;
+      if (++iy == nx && S == 7) {
+        iy = 0;
+        ++iz;
+      }
+    }
+    bool pr[S];
     if constexpr (S == 7) {
-      const unsigned iz0 = div_nx(q0, K.mg);
-      const unsigned iy0 = q0 - iz0 * nx;
-      inner = iy0 >= 1 && iy0 + 2 <= nx && iz0 >= 1 && iz0 + 2 <= nx;
+      pr[0] = iz > 0; pr[1] = iy > 0; pr[2] = ix > 0; pr[3] = true;
+      pr[4] = ix + 1 < nx; pr[5] = iy + 1 < nx; pr[6] = iz + 1 < nx;
     } else {
-      inner = q0 >= 1 && q0 + 2 <= nx;
+      pr[0] = iy > 0; pr[1] = ix > 0; pr[2] = true; pr[3] = ix + 1 < nx; pr[4] = iy + 1 < nx;
     }
-    inner = inner && ix0 >= 1 && ix0 + VN + 1 <= nx;
-    if (inner) {   // every slot present in all VN rows: p0 + (((p1 + p2) + p3) ...) directly
+    bool have = false;
+    T p0 = T(0), rest = T(-0.0);
 #pragma unroll
-      for (int e = 0; e < VN; ++e) {
-        T rest = mul_rn(K.kc[1], px[1][e]);
-#pragma unroll
-        for (int s = 2; s < S; ++s) rest = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
-        y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
-      }
-      return;
+    for (int s = 0; s < S; ++s) {
+      const T p = mul_rn(K.kc[s], px[s][e]);
+      const T nrest = add_rn(rest, p);
+      rest = (pr[s] && have) ? nrest : rest;
+      p0 = (pr[s] && !have) ? p : p0;
+      have = have || pr[s];
     }
-#pragma unroll
-    for (int e = 0; e < VN; ++e) {   // boundary groups: per-row presence, no value registers
-      const unsigned ur = ur0 + (unsigned)e;
-      const unsigned q = div_nx(ur, K.mg);
-      const unsigned ix = ur - q * nx;
-      bool pr[S];
-      if constexpr (S == 7) {
-        const unsigned iz = div_nx(q, K.mg);
-        const unsigned iy = q - iz * nx;
-        pr[0] = iz > 0; pr[1] = iy > 0; pr[2] = ix > 0; pr[3] = true;
-        pr[4] = ix + 1 < nx; pr[5] = iy + 1 < nx; pr[6] = iz + 1 < nx;
-      } else {
-        pr[0] = q > 0; pr[1] = ix > 0; pr[2] = true; pr[3] = ix + 1 < nx; pr[4] = q + 1 < nx;
-      }
-      bool have = false;
-      T p0 = T(0), rest = T(-0.0);
-#pragma unroll
-      for (int s = 0; s < S; ++s) {
-        const T p = mul_rn(K.kc[s], px[s][e]);
-        const T nrest = add_rn(rest, p);
-        rest = (pr[s] && have) ? nrest : rest;
-        p0 = (pr[s] && !have) ? p : p0;
-        have = have || pr[s];
-      }
-      y[e] = add_rn(p0, rest);
-    }
+    y[e] = add_rn(p0, rest);
   }
 }
 

@@ -428,8 +428,21 @@ __global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __re
   spmv_pipeline(A, x, epi, sm);
 }
 
+// stencil kernels: CTAs per SM the register budget must allow.  fp32 streaming
+// epilogues (SpMV, polynomial steps): 4 (<= 64 registers; measured at 400^3:
+// SpMV 189 -> 134 us, cfg4 IR + poly(25) 0.207 -> 0.165 s); fp64 and the
+// fused-dot epilogues keep the compiler's choice (forcing 4 spills 100-270 B
+// and slowed the fp64 residual 552 -> 635 us).  MPG_ST_MINB overrides (A/B).
 template <typename T, typename E>
-__global__ void __launch_bounds__(kSpConsumers) k_stencil(StencilView<T> S, const T* __restrict__ x,
+constexpr int st_minb() {
+#ifdef MPG_ST_MINB
+  return MPG_ST_MINB;
+#else
+  return sizeof(T) == 4 && !needs_tiles<E>::value ? 4 : 1;
+#endif
+}
+template <typename T, typename E>
+__global__ void __launch_bounds__(kSpConsumers, st_minb<T, E>()) k_stencil(StencilView<T> S, const T* __restrict__ x,
                                                           E epi) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ EpiShared<T> es;

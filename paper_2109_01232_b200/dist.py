@@ -24,6 +24,7 @@ restart bookkeeping (solvers.py:177-227 / :297-384).
 from __future__ import annotations
 
 import ctypes as C
+from contextlib import contextmanager
 from dataclasses import dataclass
 
 import numpy as np
@@ -316,21 +317,54 @@ class DistributedStencilSolver:
         return self.x_buf[o:o + self.part.n_local]
 
     def _ph(self, name: str, j: int = 0, m_limit: int = 1) -> None:
+        prof = getattr(self, "_prof", None)
+        if prof is not None:
+            with prof.scope(_PHASE_CLASS.get(name, "cycle"), j):
+                _lib.call("mpg_solver_phase", self.handle, PH[name], j, max(1, m_limit), stream_handle())
+            return
         _lib.call("mpg_solver_phase", self.handle, PH[name], j, max(1, m_limit), stream_handle())
+
+    def _allreduce(self, t: torch.Tensor) -> None:
+        prof = getattr(self, "_prof", None)
+        if prof is not None:
+            with prof.scope("allreduce", 0):
+                self.coll.allreduce_(t)
+            return
+        self.coll.allreduce_(t)
+
+    def _halo(self, row: torch.Tensor) -> None:
+        prof = getattr(self, "_prof", None)
+        if prof is not None:
+            with prof.scope("halo", 0):
+                self.coll.halo_(row, self.part)
+            return
+        self.coll.halo_(row, self.part)
+
+    def profile_cycle(self, m_limit: int) -> dict:
+        """One eager cycle with CUDA events around every phase and collective:
+        {class: {"ms", "launches", "bytes"}} with this rank's algorithmic bytes
+        per class (local rows)."""
+        self._prof = _CycleProfile()
+        try:
+            self._enqueue_cycle(m_limit)
+            torch.cuda.synchronize()
+        finally:
+            prof, self._prof = self._prof, None
+        return prof.result(self.part.n_local, self.prec.dtype.itemsize)
 
     # --- the distributed cycle
     def begin(self) -> tuple[float, float]:
         self._ph("BNORM")
-        self.coll.allreduce_(self.reserved0)
+        self._allreduce(self.reserved0)
         self._ph("POST_BNORM")
         self._residual()
         hdr, _ = self.state.read()
         return float(hdr.outer_b_norm), float(hdr.rnorm)
 
     def _residual(self) -> None:
-        self.coll.halo_(self.x_buf, self.part)
+        self._halo(self.x_buf)
         self._ph("RESID")
-        self.coll.allreduce_(self.reserved0)
+        self._allreduce(self.reserved0)
         self._ph("POST_RESID")
 
     def cycle(self, m_limit: int):
@@ -368,24 +402,68 @@ class DistributedStencilSolver:
 
     def _enqueue_cycle(self, m_limit: int) -> None:
         self._ph("START", 0, m_limit)
-        self.coll.allreduce_(self.red[:2])
+        self._allreduce(self.red[:2])
         self._ph("POST_START", 0, m_limit)
         self._ph("START_SCALE", 0, m_limit)
         for j in range(m_limit):
             if j == 0 or not self.peer:      # with peer halos SCALE has already written them
-                self.coll.halo_(self.V_row(j), self.part)
+                self._halo(self.V_row(j))
             self._ph("SPMV_DOT", j, m_limit)
-            self.coll.allreduce_(self.red[: j + 3])
+            self._allreduce(self.red[: j + 3])
             self._ph("POST_DOT1", j, m_limit)
             self._ph("UPDATE_DOT", j, m_limit)
-            self.coll.allreduce_(self.red[: j + 1])
+            self._allreduce(self.red[: j + 1])
             self._ph("POST_DOT2", j, m_limit)
             self._ph("UPDATE_NORM", j, m_limit)
-            self.coll.allreduce_(self.red[:1])
+            self._allreduce(self.red[:1])
             self._ph("POST_NORM", j, m_limit)
             self._ph("SCALE", j, m_limit)
         self._ph("FINISH", 0, m_limit)
         self._residual()
+
+
+# phase -> profile class (DistributedStencilSolver.profile_cycle)
+_PHASE_CLASS = {"SPMV_DOT": "spmv_dot", "UPDATE_DOT": "update_dot", "UPDATE_NORM": "update_norm",
+                "SCALE": "scale", "POST_DOT1": "post", "POST_DOT2": "post", "POST_NORM": "post"}
+
+
+class _CycleProfile:
+    """Event pairs per (class, Arnoldi step) of one eager distributed cycle."""
+
+    def __init__(self):
+        self.ev: list = []
+
+    @contextmanager
+    def scope(self, cls: str, j: int):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        try:
+            yield
+        finally:
+            e1.record()
+            self.ev.append((cls, j, e0, e1))
+
+    def result(self, n: int, s: int) -> dict:
+        # algorithmic bytes per launch of each class at step j (k = j + 1 basis
+        # vectors), this rank's rows: the constant-coefficient SpMV streams x once
+        # and writes w; the pass-1 dots read V[0..k) and w
+        def nbytes(cls, j):
+            k = j + 1
+            return {"spmv_dot": (2 + k + 1) * n * s, "update_dot": (k + 2) * n * s,
+                    "update_norm": (k + 2) * n * s, "scale": 2 * n * s}.get(cls, 0)
+        out: dict = {}
+        for cls, j, e0, e1 in self.ev:
+            ms = e0.elapsed_time(e1)
+            d = out.setdefault(cls, {"ms": 0.0, "launches": 0, "bytes": 0})
+            d["ms"] += ms
+            d["launches"] += 1
+            d["bytes"] += nbytes(cls, j)
+        for d in out.values():
+            d["ms"] = round(d["ms"], 4)
+            if d["bytes"] and d["ms"] > 0:
+                d["GBps"] = round(d["bytes"] / (d["ms"] / 1e3) / 1e9, 1)
+        return out
 
 
 def _dist_solve(solver: DistributedStencilSolver, criteria: StopCriteria, ir: bool,
