@@ -355,6 +355,10 @@ __device__ __forceinline__ T row_reduce(const Get& get, int len) {
 // visible; a no-op for a normal launch), and lets its own successor launch
 // early with pdl_trigger().  Every kernel launched with launch_k(pdl = true)
 // calls pdl_wait() before it reads anything a predecessor wrote.
+// Prefetch the 128-byte line holding p into L2 (no register, no scoreboard).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // Bulk (TMA-engine) prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2.
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

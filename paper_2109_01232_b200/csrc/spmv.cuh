@@ -345,7 +345,8 @@ __device__ __forceinline__ void xwindow(const T* __restrict__ p, int mis, T (&o)
 // selects: bit-exact.
 // The x operands of one row group (stencil_group's loads, issued together):
 // px[s][e] = x[r0 + e + off[s]].
-template <typename T, int S>
+// ALN: every neighbour window is 16-byte aligned (nx % VN == 0; mis all 0)
+template <typename T, int S, bool ALN = false>
 __device__ __forceinline__ void stencil_xload(const T* __restrict__ x, long long r0, const long long (&off)[S],
                                               const int (&mis)[S], T (&px)[S][Vec<T>::n]) {
   constexpr int VN = Vec<T>::n;
@@ -354,7 +355,10 @@ __device__ __forceinline__ void stencil_xload(const T* __restrict__ x, long long
   const T xm = __ldg(x + r0 - 1), xp = __ldg(x + r0 + VN);
 #pragma unroll
   for (int s = 0; s < S; ++s)
-    if (s < C - 1 || s > C + 1) xwindow(x + r0 + off[s], mis[s], px[s]);
+    if (s < C - 1 || s > C + 1) {
+      if (ALN) vload(x + r0 + off[s], px[s]);
+      else xwindow(x + r0 + off[s], mis[s], px[s]);
+    }
   px[C - 1][0] = xm;
 #pragma unroll
   for (int e = 1; e < VN; ++e) px[C - 1][e] = px[C][e - 1];
@@ -368,7 +372,7 @@ __device__ __forceinline__ void stencil_const_rows(const StencilView<T>& SV, lon
                                                    const StencilConst<T, S>& K, const T (&px)[S][Vec<T>::n],
                                                    T (&y)[Vec<T>::n]);
 
-template <typename T, int S>
+template <typename T, int S, bool ALN = false>
 __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T* __restrict__ x,
                                               long long r0, const long long (&off)[S],
                                               const int (&mis)[S], const StencilConst<T, S>& K,
@@ -380,7 +384,7 @@ __device__ __forceinline__ void stencil_group(const StencilView<T>& SV, const T*
 #pragma unroll
     for (int s = 0; s < S; ++s) vload(SV.vals + s * ld + r0, pv[s]);
   }
-  stencil_xload<T, S>(x, r0, off, mis, px);
+  stencil_xload<T, S, ALN>(x, r0, off, mis, px);
   if (K.on) {
     stencil_const_rows<T, S>(SV, r0, K, px, y);
     return;
@@ -433,25 +437,23 @@ __device__ __forceinline__ void stencil_const_rows(const StencilView<T>& SV, lon
     iy0 = q0;
     yz = q0 >= 1 && q0 + 2 <= nx;
   }
-  if (yz && ix0 >= 1 && ix0 + VN + 1 <= nx) {   // interior
-#pragma unroll
-    for (int e = 0; e < VN; ++e) {
-      T rest = mul_rn(K.kc[1], px[1][e]);
-#pragma unroll
-      for (int s = 2; s < S; ++s) rest = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
-      y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
-    }
-    return;
-  }
-  if (yz && ix0 + VN <= nx) {   // x-boundary group within one x-line
+  if (yz && ix0 + VN <= nx) {
+    // the group lies in one x-line inside the y/z interior: only the x-1 / x+1
+    // slots can be absent (first / last row of the line), both inside the
+    // "rest" chain, so they are skipped with a predicated add and p0 stays the
+    // z-1 (2-D: y-1) product.  One code path for interior and x-boundary
+    // groups: no warp divergence at the ends of the x-lines.
 #pragma unroll
     for (int e = 0; e < VN; ++e) {
       const unsigned ix = ix0 + (unsigned)e;
-      T rest = T(-0.0);   // (2-D: the x-1 slot is p1 itself)
+      const bool hm = ix > 0, hp = ix + 1 < nx;
+      T rest;
+      if constexpr (S == 7) rest = mul_rn(K.kc[1], px[1][e]);   // y-1: present
+      else rest = hm ? mul_rn(K.kc[1], px[1][e]) : T(-0.0);    // x-1 is p1 in 2-D
 #pragma unroll
-      for (int s = 1; s < S; ++s) {
+      for (int s = 2; s < S; ++s) {
         const T nr = add_rn(rest, mul_rn(K.kc[s], px[s][e]));
-        rest = s == XM ? (ix > 0 ? nr : rest) : (s == XP ? (ix + 1 < nx ? nr : rest) : nr);
+        rest = s == XM ? (hm ? nr : rest) : (s == XP ? (hp ? nr : rest) : nr);
       }
       y[e] = add_rn(mul_rn(K.kc[0], px[0][e]), rest);
     }
@@ -497,7 +499,7 @@ __device__ __forceinline__ void stencil_mis(const long long (&off)[S], int (&mis
 
 // Vectorised branchless stencil rows on padded inputs: each consumer thread
 // owns one 16-byte group of VN consecutive rows per tile (stencil_group).
-template <typename T, int S, typename E>
+template <typename T, int S, typename E, bool ALN = false>
 __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const T* __restrict__ x,
                                                  const long long (&off)[S], E& epi,
                                                  EpiShared<T>& es) {
@@ -507,6 +509,37 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
   int mis[S];
   stencil_mis<T, S>(off, mis);
   const StencilConst<T, S> K = stencil_const<T, S>(SV);
+  if constexpr (!needs_tiles<E>::value) {
+    // grid-stride over 16-byte row groups (the same rows per thread as the
+    // tiled loop below: tile blockIdx.x + t * gridDim.x, group threadIdx.x)
+    const long long stride = (long long)gridDim.x * TILE;
+    T* ysp = es.ys[0] + threadIdx.x * VN;   // on_row scratch, never read back
+    // the leading-edge window x[r0 + off[S-1]] (the +nx^2 / +nx neighbour) is the
+    // only load of a group that misses L2 -- the other windows were the leading
+    // edge of an earlier group -- so the thread prefetches the next iterations'
+    // leading edges into L2 (MPG_ST_PF iterations ahead; 0 disables)
+    // (measured at 400^3: fp64 SpMV 363 -> 287 us, residual 594 -> 526 us; fp32
+    // 120 -> 124 us, so fp32 does not prefetch)
+#ifndef MPG_ST_PF32
+#define MPG_ST_PF32 0
+#endif
+#ifndef MPG_ST_PF64
+#define MPG_ST_PF64 2
+#endif
+    constexpr int PF = sizeof(T) == 8 ? MPG_ST_PF64 : MPG_ST_PF32;
+#pragma unroll 1
+    for (long long r0 = ((long long)blockIdx.x * kSpConsumers + threadIdx.x) * VN; r0 < n; r0 += stride) {
+      if (PF > 0) {
+        const long long pf = r0 + PF * stride + off[S - 1];
+        if (pf < n + off[S - 1] && (threadIdx.x & 7) == 0) prefetch_l2(x + pf);   // one lane per 128 B
+      }
+      T y[VN];
+      stencil_group<T, S, ALN>(SV, x, r0, off, mis, K, y);
+      epi_rows(epi, r0, y, (int)min((long long)VN, n - r0), ysp);
+    }
+    epi.on_end();
+    return;
+  }
   const long long ntiles = (n + TILE - 1) / TILE;
   int t = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
@@ -528,17 +561,17 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
   epi.on_end();
 }
 
-template <typename T, typename E>
+template <typename T, typename E, bool ALN = false>
 __device__ __forceinline__ void stencil_pipeline(const StencilView<T>& S, const T* __restrict__ x,
                                                  E& epi, EpiShared<T>& es) {
   if (S.padded) {
     const long long nx = S.nx, p2 = nx * nx;
     if (S.dims == 3) {
       const long long off[7] = {-p2, -nx, -1, 0, 1, nx, p2};
-      stencil_loop_vec<T, 7>(S, x, off, epi, es);
+      stencil_loop_vec<T, 7, E, ALN>(S, x, off, epi, es);
     } else {
       const long long off[5] = {-nx, -1, 0, 1, nx};
-      stencil_loop_vec<T, 5>(S, x, off, epi, es);
+      stencil_loop_vec<T, 5, E, ALN>(S, x, off, epi, es);
     }
   } else {
     stencil_loop(S.n, epi, es, [&](long long r) { return stencil_row<T>(S, x, r); });

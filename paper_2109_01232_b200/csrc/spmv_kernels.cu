@@ -429,19 +429,21 @@ __global__ void __launch_bounds__(kSpThreads) k_spmv(CsrView<T> A, const T* __re
 }
 
 // stencil kernels: CTAs per SM the register budget must allow.  fp32 streaming
-// epilogues (SpMV, polynomial steps): 4 (<= 64 registers; measured at 400^3:
-// SpMV 189 -> 134 us, cfg4 IR + poly(25) 0.207 -> 0.165 s); fp64 and the
-// fused-dot epilogues keep the compiler's choice (forcing 4 spills 100-270 B
-// and slowed the fp64 residual 552 -> 635 us).  MPG_ST_MINB overrides (A/B).
+// epilogues (SpMV, residual, polynomial steps): 4 (<= 64 registers; measured
+// at 400^3: SpMV 189 -> 134 us, cfg4 IR + poly(25) 0.207 -> 0.165 s); fp64: 2
+// (<= 128 registers, no spills); the fused-dot epilogues keep the compiler's
+// choice.  MPG_ST_MINB32 / MPG_ST_MINB64 override (A/B).
+#ifndef MPG_ST_MINB32
+#define MPG_ST_MINB32 4
+#endif
+#ifndef MPG_ST_MINB64
+#define MPG_ST_MINB64 2
+#endif
 template <typename T, typename E>
 constexpr int st_minb() {
-#ifdef MPG_ST_MINB
-  return MPG_ST_MINB;
-#else
-  return sizeof(T) == 4 && !needs_tiles<E>::value ? 4 : 1;
-#endif
+  return needs_tiles<E>::value ? 1 : (sizeof(T) == 4 ? MPG_ST_MINB32 : MPG_ST_MINB64);
 }
-template <typename T, typename E>
+template <typename T, typename E, bool ALN>
 __global__ void __launch_bounds__(kSpConsumers, st_minb<T, E>()) k_stencil(StencilView<T> S, const T* __restrict__ x,
                                                           E epi) {
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(kSpConsumers, st_minb<T, E>()) k_stencil(Stenc
   if (epi.skip()) return;
   epi.mark();
   epi.init(es, smraw);
-  stencil_pipeline(S, x, epi, es);
+  stencil_pipeline<T, E, ALN>(S, x, epi, es);
 }
 
 // ------------------------------------------------------------------------
@@ -774,15 +776,15 @@ static cudaError_t launch_matrix(const CsrView<T>& A, const T* x, const E& epi, 
   return launch_k(E::kPdl, false, k_spmv<T, E>, dim3((unsigned)G), dim3(kSpThreads), smem, st, A, x, epi);
 }
 
-template <typename T, typename E>
-static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& epi, size_t extra,
-                                 cudaStream_t st) {
+template <typename T, typename E, bool ALN>
+static cudaError_t launch_stencil_k(const StencilView<T>& S, const T* x, const E& epi, size_t extra,
+                                    cudaStream_t st) {
   static std::once_flag once;
   static int occ = 1;
   std::call_once(once, [&] {
-    cudaFuncSetAttribute(k_stencil<T, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_stencil<T, E, ALN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)((size_t)(kMaxM + 8) * sizeof(T) * 8));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<T, E>, kSpConsumers, extra);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stencil<T, E, ALN>, kSpConsumers, extra);
     cudaGetLastError();
     if (occ < 1) occ = 1;
   });
@@ -794,7 +796,19 @@ static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& e
   if (G > kMaxParts) G = kMaxParts;
   if (G < 1) G = 1;
   count_launch();
-  return launch_k(E::kPdl, false, k_stencil<T, E>, dim3((unsigned)G), dim3(kSpConsumers), extra, st, S, x, epi);
+  return launch_k(E::kPdl, false, k_stencil<T, E, ALN>, dim3((unsigned)G), dim3(kSpConsumers), extra, st, S, x, epi);
+}
+
+// Aligned instantiation when every neighbour window is 16-byte aligned
+// (nx % VN == 0: no misaligned-window code in the loop) for the streaming
+// epilogues; the tile (fused-dot) epilogues keep the general one.
+template <typename T, typename E>
+static cudaError_t launch_matrix(const StencilView<T>& S, const T* x, const E& epi, size_t extra,
+                                 cudaStream_t st) {
+  if constexpr (!needs_tiles<E>::value) {
+    if (S.padded && S.nx % Vec<T>::n == 0) return launch_stencil_k<T, E, true>(S, x, epi, extra, st);
+  }
+  return launch_stencil_k<T, E, false>(S, x, epi, extra, st);
 }
 
 template <typename T, typename M>

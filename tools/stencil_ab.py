@@ -23,6 +23,15 @@ for nx in (400, 150):
     print(json.dumps({"lib": tag, "nx": nx, "spmv_us": round(sp[0] / sp[1] * 1e3, 2),
                       "spmv_TBs": round(2 * n * 4 / (sp[0] / sp[1] * 1e-3) / 1e12, 3),
                       "resid64_us": round(res[0] * 1e3, 1), "resid64_TBs": round(3 * n * 8 / (res[0] * 1e-3) / 1e12, 3)}))
+    with P.solvers.step_kernel("split"):
+        ns = NativeSolve(_lib.MODE_RESTARTED, FP64, A, None, padded_copy(b, FP64), dvec(n, FP64), 50, 1e-10)
+    ns.begin(); ns.cycle(50)
+    prof = ns.profile_cycle(50)
+    ns.close()
+    sp = prof["spmv_dot1"]
+    print(json.dumps({"lib": tag, "nx": nx, "fp64_spmv_us": round(sp[0] / sp[1] * 1e3, 2),
+                      "fp64_spmv_TBs": round(2 * n * 8 / (sp[0] / sp[1] * 1e-3) / 1e12, 3),
+                      "fp64_resid_us": round(prof["residual"][0] * 1e3, 1)}))
     del A, b
     torch.cuda.empty_cache()
 A = P.generate(P.StencilSpec(P.StencilKind.LAPLACE3D, 200))
