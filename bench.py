@@ -355,7 +355,7 @@ def _max_over_ranks_profile(prof: dict) -> dict:
 def _dist_roofline(prof: dict) -> dict | None:
     """Roofline of the dominant phase kernel class of a distributed cycle
     (algorithmic bytes of this rank's rows / device time, max over ranks)."""
-    cls = [k for k in ("spmv_dot", "update_dot", "update_norm", "scale") if k in prof and prof[k].get("GBps")]
+    cls = [k for k in ("step", "spmv_dot", "update_dot", "update_norm", "scale") if k in prof and prof[k].get("GBps")]
     if not cls:
         return None
     dom = max(cls, key=lambda k: prof[k]["ms"])
@@ -421,7 +421,7 @@ def cfg5_segment_single() -> dict:
     return out
 
 
-def cfg5_segment_dist(world: int, rank: int, coll, peer: bool) -> dict:
+def cfg5_segment_dist(world: int, rank: int, coll, peer: bool, persistent: bool = True) -> dict:
     """BASELINE configs[4] row-partitioned over the ranks: GMRES-IR for a fixed
     two restart cycles of Laplace3D 400^3, s/iteration (max over ranks), the
     profiled cycle's per-phase GB/s and communication share."""
@@ -432,7 +432,7 @@ def cfg5_segment_dist(world: int, rank: int, coll, peer: bool) -> dict:
     spec = P.StencilSpec(P.StencilKind.LAPLACE3D, CFG5_NX)
     part = RowPartition.for_stencil(3, CFG5_NX, world, rank)
     crit = StopCriteria(rtol=RTOL, m=M, max_iters=CFG5_ITERS)
-    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer)
+    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer, persistent=persistent)
     try:
         solver.x_buf.zero_()
         _dist_solve(solver, crit, True, None)                 # warm (graphs captured)
@@ -506,7 +506,11 @@ def dist_arm(args, rank: int, world: int):
     crit = StopCriteria(rtol=RTOL, m=M)
     # NVLink peer-memory halos written by the SCALE phase (MPG_PEER_HALO=0: NCCL send/recv)
     peer = os.environ.get("MPG_PEER_HALO", "1") != "0"
-    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer)
+    # one cooperative kernel per Arnoldi step with the cross-rank sums done
+    # in-kernel over peer memory (MPG_DIST_PERSISTENT=0: the phase path, NCCL
+    # allreduces between per-phase kernels)
+    pers = os.environ.get("MPG_DIST_PERSISTENT", "1") != "0"
+    solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer, persistent=pers)
 
     def solve():
         solver.x_buf.zero_()
@@ -533,7 +537,7 @@ def dist_arm(args, rank: int, world: int):
     solver.x_buf.zero_()
     solver.begin()
     prof = _max_over_ranks_profile(solver.profile_cycle(M))
-    cfg5 = cfg5_segment_dist(world, rank, coll, peer)
+    cfg5 = cfg5_segment_dist(world, rank, coll, peer, pers)
     # e2e: public distributed API with a host right-hand side slice, x downloaded
     b_host = np.ones(part.n_local)
     torch.distributed.barrier()
@@ -556,9 +560,13 @@ def dist_arm(args, rank: int, world: int):
         "config": {"workload": "gmres_ir laplace3d:150 GMRES(50) rtol=1e-10 (BASELINE configs[1]), "
                                "row-partitioned by z-planes",
                    "n": NX ** 3, "m": M, "rtol": RTOL, "parallelism": f"rows{world}",
-                   "collectives": ("peer-memory halo stores fused into the basis scaling + " if solver.peer
-                                   else "NCCL halo send/recv + ") + "3 NCCL allreduces per Arnoldi step; "
-                                  "whole cycles replayed as CUDA graphs",
+                   "collectives": ("one cooperative kernel per Arnoldi step per rank: the three cross-rank "
+                                   "sums done in-kernel over peer-memory exchange boxes (release/acquire "
+                                   "sequence numbers), halo planes stored into the neighbours by the kernel; "
+                                   "NCCL only for the per-cycle start/residual sums" if solver.persistent else
+                                   ("peer-memory halo stores fused into the basis scaling + " if solver.peer
+                                    else "NCCL halo send/recv + ") + "3 NCCL allreduces per Arnoldi step")
+                                  + "; whole cycles replayed as CUDA graphs",
                    "l2": "working set >> L2 per rank at N<=8; no flush needed"},
         "iters": rep.total_iters, "iters_reference": REFERENCE_IR_ITERS,
         "storage": "stencil", "gpu_launches": launches, "clocks": clk.summary(),

@@ -328,7 +328,19 @@ typedef struct {
   uint32_t* halo_flags;     /* this rank's 2 flags: [0] written by prev, [1] by next */
   uint32_t* peer_prev_flag; /* the prev rank's halo_flags + 1 */
   uint32_t* peer_next_flag; /* the next rank's halo_flags + 0 */
+  /* Distributed persistent step (MPG_PH_STEP): one cooperative kernel per
+   * Arnoldi step per rank that also does the step's three cross-rank sums
+   * over peer memory.  Every rank owns an exchange box of
+   * mpg_xbox_bytes() bytes (zeroed once); xbox[r] is rank r's box as mapped
+   * in this process (xbox[xrank] = this rank's own), r < xworld <= 8.  The
+   * peer-memory halo fields above must be set for xworld > 1. */
+  int32_t xworld;           /* 0: no in-kernel exchange (phase path only) */
+  int32_t xrank;
+  void* xbox[8];
 } mpg_solver_desc;
+
+/* Bytes of one rank's exchange box for the distributed persistent step. */
+int64_t mpg_xbox_bytes(void);
 
 /* Phases of one distributed restart cycle.  A phase marked
  * "raw" leaves this rank's partial sums in the state (red[] in the working
@@ -350,6 +362,10 @@ typedef struct {
 #define MPG_PH_POST_NORM 12
 #define MPG_PH_SCALE 13
 #define MPG_PH_FINISH 14      /* back-solve (replicated) + local solution update   */
+#define MPG_PH_STEP 15        /* the whole Arnoldi step j in one cooperative kernel:
+                                 SPMV_DOT .. SCALE with the three cross-rank sums
+                                 done in-kernel over the exchange boxes (needs
+                                 xworld >= 1; halo(V[:,0]) before j = 0 only)  */
 
 typedef struct mpg_solver mpg_solver;
 

@@ -69,7 +69,8 @@ class SolverDesc(C.Structure):
                 ("halo", C.c_int64), ("dia_ld", C.c_int64),
                 ("peer_prev_V", C.c_void_p), ("peer_prev_ld", C.c_int64), ("peer_prev_off", C.c_int64),
                 ("peer_next_V", C.c_void_p), ("peer_next_ld", C.c_int64), ("peer_next_off", C.c_int64),
-                ("halo_flags", C.c_void_p), ("peer_prev_flag", C.c_void_p), ("peer_next_flag", C.c_void_p)]
+                ("halo_flags", C.c_void_p), ("peer_prev_flag", C.c_void_p), ("peer_next_flag", C.c_void_p),
+                ("xworld", C.c_int32), ("xrank", C.c_int32), ("xbox", C.c_void_p * 8)]
 
 
 _vp, _i32, _i64, _d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
@@ -77,6 +78,7 @@ _SIGS = {
     "mpg_version": (C.c_char_p, []),
     "mpg_workspace_bytes": (_i64, []),
     "mpg_solver_desc_bytes": (_i64, []),
+    "mpg_xbox_bytes": (_i64, []),
     "mpg_launch_count": (_i64, []),
     "mpg_spmv": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mpg_residual": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

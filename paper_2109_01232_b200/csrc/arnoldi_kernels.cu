@@ -744,14 +744,6 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
 // `halo` rows to next's lower halo.  After every CTA's stores are fenced
 // system-wide, the last CTA bumps this rank's halo sequence number (header
 // reserved1) and release-stores it into both neighbours' flags.
-__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_step_scale_peer(const T* __restrict__ w, T* __restrict__ vn,

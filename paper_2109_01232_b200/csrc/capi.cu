@@ -20,6 +20,7 @@ extern "C" {
 const char* mpg_version(void) { return "mpgmres_b200 0.1.0 sm_100a"; }
 int64_t mpg_workspace_bytes(void) { return kWsBytes; }
 int64_t mpg_solver_desc_bytes(void) { return (int64_t)sizeof(mpg_solver_desc); }
+int64_t mpg_xbox_bytes(void) { return kXBoxBytes; }
 int64_t mpg_launch_count(void) { return g_launches.load(); }
 
 int mpg_spmv(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* v,

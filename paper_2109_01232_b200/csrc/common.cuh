@@ -355,6 +355,26 @@ __device__ __forceinline__ T row_reduce(const Get& get, int len) {
 // visible; a no-op for a normal launch), and lets its own successor launch
 // early with pdl_trigger().  Every kernel launched with launch_k(pdl = true)
 // calls pdl_wait() before it reads anything a predecessor wrote.
+// System-scope release / acquire (peer-memory flags across GPUs / processes).
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p >= want (wrap-safe), bounded: ~20 s of SM clock, then false.
+__device__ __forceinline__ bool wait_seq_sys(const uint32_t* p, uint32_t want) {
+  const unsigned long long t0 = clock64(), limit = 40ull * 1000 * 1000 * 1000;
+  int spins = 0;
+  while ((int32_t)(ld_acquire_sys_u32(p) - want) < 0) {
+    if (clock64() - t0 > limit) return false;
+    if (++spins > 64) __nanosleep(32);   // tight spin first: the wait is usually short
+  }
+  return true;
+}
+
 // Prefetch the 128-byte line holding p into L2 (no register, no scoreboard).
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));

@@ -389,6 +389,35 @@ static cudaError_t enqueue_phase(const mpg_solver& s, int phase, int j, int m_li
       return launch_step_scale<T>(w, V + (size_t)(j + 1) * d.ldv, d.n, j, sv, st);
     case MPG_PH_FINISH:
       return finish_cycle<T>(s, sv, ws, st);
+    case MPG_PH_STEP: {
+      // the whole Arnoldi step in one cooperative kernel, the three cross-rank
+      // sums over the exchange boxes (step_kernel.cu DIST); V[:, j]'s halo is
+      // in place (collective exchange before j = 0, peer stores after)
+      if (d.xworld < 1 || d.xworld > kXMaxRanks || !d.xbox[d.xrank] || d.pc_kind != MPG_PC_NONE)
+        return cudaErrorInvalidValue;
+      MegaX<T> X{};
+      for (int r = 0; r < d.xworld; ++r) X.box[r] = d.xbox[r];
+      X.world = d.xworld;
+      X.rank = d.xrank;
+      X.halo = d.halo;
+      if (d.xworld > 1) {
+        X.prev_V = static_cast<T*>(d.peer_prev_V);
+        X.prev_ld = d.peer_prev_ld;
+        X.prev_off = d.peer_prev_off;
+        X.next_V = static_cast<T*>(d.peer_next_V);
+        X.next_ld = d.peer_next_ld;
+        X.next_off = d.peer_next_off;
+        X.hflags = d.halo_flags;
+        X.prev_flag = d.peer_prev_flag;
+        X.next_flag = d.peer_next_flag;
+      }
+      StencilView<T> S{static_cast<const T*>(d.dia), d.dia_ld ? d.dia_ld : d.ldv, d.n, d.stencil_nx,
+                       d.stencil_dims, d.row0};
+      S.padded = 1;
+      S.konst = s.dia_const ? 2 : 0;
+      return launch_step_mega<T>(S, V + (size_t)j * d.ldv, V, d.ldv, d.n, j, w, sv, ws, m_limit, st, nullptr,
+                                 nullptr, &X);
+    }
     default:
       return cudaErrorInvalidValue;
   }
@@ -431,7 +460,7 @@ extern "C" int mpg_solver_create(const mpg_solver_desc* desc, mpg_solver** out) 
   if (d.dist && (!d.stencil_dims || d.pc_kind != MPG_PC_NONE)) return MPG_EUNSUPPORTED;
   mpg_solver* s = new mpg_solver();
   s->d = d;
-  if (d.stencil_dims && d.dia && !d.dist) {   // constant-coefficient header (spmv.cuh StencilConst)
+  if (d.stencil_dims && d.dia) {   // constant-coefficient header (spmv.cuh StencilConst)
     const int S = d.stencil_dims == 3 ? 7 : 5;
     const size_t es = d.prec == MPG_FP64 ? 8 : 4;
     const char* hp = static_cast<const char*>(d.dia) + (size_t)S * (d.dia_ld ? d.dia_ld : d.ldv) * es;

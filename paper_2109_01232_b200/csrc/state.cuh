@@ -162,6 +162,46 @@ cudaError_t launch_step_scale_peer(const T* w, T* vn, long long n, long long hal
 cudaError_t launch_halo_wait(mpg_state_header* h, const uint32_t* flags, int has_prev, int has_next,
                              cudaStream_t st);
 
+// ---------------------------------------------------------- exchange box
+// One rank's mailbox for the distributed persistent step (MPG_PH_STEP): for
+// each of the step's three cross-rank sums p (pass-1 dots + ||w||^2 + flag,
+// pass-2 dots, ||w''||^2), rank r's local column sums land in vals[p][r][:]
+// (written by rank r through its peer mapping) and rank r then release-stores
+// the step's sequence number into seq[p][r].  Sums are read back in rank
+// order, so every rank gets the same bits.  `step` counts this rank's step
+// kernels (identical on every rank).
+constexpr int kXMaxRanks = 8;
+constexpr int kXCols = 72;                                   // >= kMegaMaxCols
+constexpr int64_t kXValsBytes = (int64_t)3 * kXMaxRanks * kXCols * 8;
+constexpr int64_t kXSeqOff = kXValsBytes;                     // uint32 seq[3][kXMaxRanks]
+constexpr int64_t kXStepOff = kXSeqOff + 3 * kXMaxRanks * 4;  // uint32 step
+constexpr int64_t kXBoxBytes = kXStepOff + 256;
+template <typename T>
+__device__ __forceinline__ T* xbox_vals(void* box, int p, int r) {
+  return reinterpret_cast<T*>(static_cast<char*>(box)) + ((size_t)p * kXMaxRanks + r) * kXCols;
+}
+__device__ __forceinline__ uint32_t* xbox_seq(void* box, int p, int r) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(box) + kXSeqOff) + p * kXMaxRanks + r;
+}
+__device__ __forceinline__ uint32_t* xbox_step(void* box) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(box) + kXStepOff);
+}
+
+// The distributed persistent step's view of the peers (DIST instantiation).
+template <typename T>
+struct MegaX {
+  void* box[kXMaxRanks];   // every rank's exchange box as mapped here
+  int world, rank;
+  long long halo;          // rows of one halo plane
+  T* prev_V;               // prev rank's basis (row 0 at its owned offset) or null
+  long long prev_ld, prev_off;
+  T* next_V;
+  long long next_ld, next_off;
+  uint32_t* hflags;        // this rank's halo flags ([0] from prev, [1] from next)
+  uint32_t* prev_flag;     // where we release into prev's / next's flags
+  uint32_t* next_flag;
+};
+
 // persistent per-step kernel (step_kernel.cu), stencil storage, single GPU;
 // steps with k > kMegaMaxK basis vectors use the four-launch step
 constexpr int kMegaMaxK = 56;
@@ -170,7 +210,7 @@ constexpr int kMegaMaxK = 56;
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& S, const T* x, T* V, long long ldv, long long n, int j,
                              T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
-                             const T* jdiag = nullptr, T* zout = nullptr);
+                             const T* jdiag = nullptr, T* zout = nullptr, const MegaX<T>* xd = nullptr);
 int mega_env();   // MPG_MEGA: 1 / 0 forces the persistent / four-launch step, -1 unset
 
 // distributed-mode post phases (k_dist_post)

@@ -92,11 +92,70 @@ __device__ __forceinline__ T sum_column(const T* part, int col, int G) {
   return warp_sum(s);
 }
 
-template <typename T, int S, int KV, bool CACHE, bool KONST>
+// Distributed persistent step (DIST, MPG_PH_STEP): the same kernel on one
+// rank's rows, with each of the three reductions finished across ranks inside
+// the kernel: after the local grid barrier CTA 0 pushes this rank's column
+// sums into every rank's exchange box (peer stores) and release-stores the
+// step's sequence number; every CTA acquire-waits for all ranks' entries in
+// its own box and sums them in rank order (identical bits on every rank, and
+// bitwise the single-GPU step at one rank).  The halo planes of V[:, j+1] are
+// stored straight into the neighbours' basis rows in P4; the next step's
+// kernel releases them at entry and waits for its own.
+template <typename T>
+__device__ __forceinline__ void mega_xsum(const MegaX<T>& X, int p, int ncols, uint32_t seqv, T* col,
+                                          mpg_state_header* h) {
+  const int tid = threadIdx.x;
+  void* self = X.box[X.rank];
+  if (blockIdx.x == 0) {   // col[] holds this rank's sums (all CTAs computed them; CTA 0 sends)
+    for (int idx = tid; idx < X.world * ncols; idx += blockDim.x) {
+      const int r = idx / ncols, c = idx - r * ncols;
+      xbox_vals<T>(X.box[r], p, X.rank)[c] = col[c];
+    }
+    // bar.sync orders the CTA's value stores before the (cumulative) system-
+    // scope release of the sequence number: no separate fence.sc.sys
+    __syncthreads();
+    if (tid < X.world) st_release_sys_u32(xbox_seq(X.box[tid], p, X.rank), seqv);
+  }
+  if (tid < X.world && !wait_seq_sys(xbox_seq(self, p, tid), seqv)) {
+    atomicOr(&h->flags, MPG_FLAG_HALO_TIMEOUT);   // a rank never arrived: finish flagged, no hang
+    h->done = 1;
+  }
+  __syncthreads();
+  if (tid < ncols) {
+    T s = __ldcg(xbox_vals<T>(self, p, 0) + tid);
+    for (int r = 1; r < X.world; ++r) s += __ldcg(xbox_vals<T>(self, p, r) + tid);
+    col[tid] = s;
+  }
+  __syncthreads();
+}
+
+template <typename T, int S, int KV, bool CACHE, bool KONST, bool DIST>
 __global__ void __launch_bounds__(kMegaThreads, 1)
 k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, long long n, int j,
-            T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout) {
+            T* wg, StateView<T> sv, WsView ws, int m_limit, const T* __restrict__ jdiag, T* zout, MegaX<T> X) {
   if (gated(sv.h)) return;
+  uint32_t seqv = 0;
+  if constexpr (DIST) {
+    seqv = *(volatile const uint32_t*)xbox_step(X.box[X.rank]) + 1u;
+    if (j >= 1 && (X.prev_V || X.next_V)) {
+      // our previous step kernel stored the halo rows of V[:, j] into the
+      // neighbours (kernel boundary: complete); release them, then wait for ours
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        __threadfence_system();
+        if (X.prev_V) st_release_sys_u32(X.prev_flag, seqv);
+        if (X.next_V) st_release_sys_u32(X.next_flag, seqv);
+      }
+      if (threadIdx.x == 0) {
+        const bool ok = (!X.prev_V || wait_seq_sys(X.hflags + 0, seqv)) &&
+                        (!X.next_V || wait_seq_sys(X.hflags + 1, seqv));
+        if (!ok) {
+          atomicOr(&sv.h->flags, MPG_FLAG_HALO_TIMEOUT);
+          sv.h->done = 1;
+        }
+      }
+      __syncthreads();
+    }
+  }
   // kernel-time categories (timing.py): CTA 0 stamps at its own phase ends and
   // after each grid barrier, so each interval ends when the grid has finished
   // the phase (B1..B3) or, for the SpMV, when CTA 0 has
@@ -273,6 +332,11 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (lane == 0) c1v[c] = s;
   }
   __syncthreads();
+  if constexpr (DIST) {
+    mega_xsum<T>(X, 0, k + 2, seqv, c1v, sv.h);
+    // every CTA has read the step counter (at entry, before B1): advance it
+    if (blockIdx.x == 0 && tid == 0) *(volatile uint32_t*)xbox_step(X.box[X.rank]) = seqv;
+  }
   if (c1v[k + 1] != T(0)) {   // non-finite operator output (krylov.py:131-133): every CTA agrees
     if (blockIdx.x == 0 && tid == 0) {
       sv.h->flags |= MPG_FLAG_NONFINITE_OP;
@@ -393,6 +457,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (lane == 0) c2v[c] = s;
   }
   __syncthreads();
+  if constexpr (DIST) mega_xsum<T>(X, 1, k, seqv, c2v, sv.h);
   if (kt0) kt_stamp(sv.h, KC_GEMV_N);                    // P3: w'' = w' - V c2
   if (blockIdx.x == 0 && tid < k) {
     sv.c2[tid] = c2v[tid];
@@ -459,6 +524,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (lane == 0) red[0] = s;
   }
   __syncthreads();
+  if constexpr (DIST) mega_xsum<T>(X, 2, 1, seqv, red, sv.h);
   const T hs = sqrt_rn(red[0]);
   if (kt0) kt_stamp(sv.h, KC_OTHER);                     // Givens + V[:, j+1] = w'' / h
   const bool brk = (double)hs <= sv.h->breakdown_tol * w0;   // krylov.py:146
@@ -483,6 +549,20 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
 #pragma unroll
     for (int e = 0; e < VN; ++e) a[e] = div_rn(a[e], hs);   // rows >= n stay 0
     vstore(vn + r, a);
+    if constexpr (DIST) {   // the halo planes of V[:, j+1], straight into the neighbours' rows
+      if (X.prev_V && r < X.halo) {
+        T* d = X.prev_V + (size_t)(j + 1) * X.prev_ld + X.prev_off;
+#pragma unroll
+        for (int e = 0; e < VN; ++e)
+          if (r + e < X.halo) d[r + e] = a[e];
+      }
+      if (X.next_V && r + VN > n - X.halo) {
+        T* d = X.next_V + (size_t)(j + 1) * X.next_ld + X.next_off - (n - X.halo);
+#pragma unroll
+        for (int e = 0; e < VN; ++e)
+          if (r + e >= n - X.halo && r + e < n) d[r + e] = a[e];
+      }
+    }
     if (jdiag) {   // Jacobi(1): the next step's operator input z = v / diag (precond.py:384-390)
       if (r + VN <= n) {
         T dv[VN];
@@ -494,6 +574,9 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
         for (int e = 0; r + e < n; ++e) zout[r + e] = div_rn(a[e], __ldg(jdiag + r + e));
       }
     }
+  }
+  if constexpr (DIST) {   // this CTA's peer halo stores are system-visible before the kernel ends
+    if (X.prev_V || X.next_V) __threadfence_system();
   }
   __syncthreads();
   MEGA_STAMP(8)
@@ -518,28 +601,28 @@ int mega_env() {
   return v;
 }
 
-template <typename T, int S, int KV, bool CACHE, bool KONST>
+template <typename T, int S, int KV, bool CACHE, bool KONST, bool DIST>
 static cudaError_t launch_mega_k(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
                                  int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
-                                 unsigned grid, size_t smem, const T* jdiag, T* zout) {
+                                 unsigned grid, size_t smem, const T* jdiag, T* zout, const MegaX<T>& X) {
   static std::once_flag once;
   std::call_once(once, [] {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE, KONST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_step_mega<T, S, KV, CACHE, KONST, DIST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          optin - (int)sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * 32 * Vec<T>::n + 3 * kMegaMaxCols * 2) - 2048);
     cudaGetLastError();
   });
   count_launch();
-  return launch_k(false, true, k_step_mega<T, S, KV, CACHE, KONST>, dim3(grid), dim3(kMegaThreads), smem, st, SV, x,
-                  V, ldv, n, j, w, sv, ws, m_limit, jdiag, zout);
+  return launch_k(false, true, k_step_mega<T, S, KV, CACHE, KONST, DIST>, dim3(grid), dim3(kMegaThreads), smem, st,
+                  SV, x, V, ldv, n, j, w, sv, ws, m_limit, jdiag, zout, X);
 }
 
-template <typename T, int S, int KV>
+template <typename T, int S, int KV, bool DIST>
 static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n,
                                   int j, T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st,
-                                  const T* jdiag, T* zout) {
+                                  const T* jdiag, T* zout, const MegaX<T>& X) {
   constexpr int RB = 32 * Vec<T>::n;
   const long long nblk = (n + RB - 1) / RB;
   const long long G = std::min<long long>(num_sms(), nblk);
@@ -554,27 +637,33 @@ static cudaError_t launch_mega_kv(const StencilView<T>& SV, const T* x, T* V, lo
   const size_t stat = sizeof(T) * (kMegaGroups * 9 * MegaU<T, KV>::u * RB + 3 * kMegaMaxCols * 2) + 2048;
   if (cache + stat <= (size_t)optin) {
     if (SV.konst == 2)
-      return launch_mega_k<T, S, KV, true, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache,
-                                                 jdiag, zout);
-    return launch_mega_k<T, S, KV, true, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, cache,
-                                                jdiag, zout);
+      return launch_mega_k<T, S, KV, true, true, DIST>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G,
+                                                       cache, jdiag, zout, X);
+    return launch_mega_k<T, S, KV, true, false, DIST>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G,
+                                                      cache, jdiag, zout, X);
   }
-  return launch_mega_k<T, S, KV, false, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0, jdiag,
-                                               zout);
+  return launch_mega_k<T, S, KV, false, false, DIST>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, (unsigned)G, 0,
+                                                     jdiag, zout, X);
 }
 
 template <typename T>
 cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long long ldv, long long n, int j,
                              T* w, StateView<T> sv, WsView ws, int m_limit, cudaStream_t st, const T* jdiag,
-                             T* zout) {
+                             T* zout, const MegaX<T>* xd) {
   const int k = j + 1;
   if (k > kMegaMaxK || k + 2 > kMegaMaxCols || !SV.padded) return cudaErrorInvalidValue;
+  if (xd && (xd->world < 1 || xd->world > kXMaxRanks || jdiag)) return cudaErrorInvalidValue;
   const int kv = (k + 7) / 8;
+  const MegaX<T> X = xd ? *xd : MegaX<T>{};
 #define MEGA_CASE(KVV)                                                                            \
   case KVV:                                                                                       \
+    if (xd)                                                                                       \
+      return SV.dims == 3                                                                         \
+                 ? launch_mega_kv<T, 7, KVV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout, X) \
+                 : launch_mega_kv<T, 5, KVV, true>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout, X); \
     return SV.dims == 3                                                                           \
-               ? launch_mega_kv<T, 7, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout)  \
-               : launch_mega_kv<T, 5, KVV>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout);
+               ? launch_mega_kv<T, 7, KVV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout, X) \
+               : launch_mega_kv<T, 5, KVV, false>(SV, x, V, ldv, n, j, w, sv, ws, m_limit, st, jdiag, zout, X);
   switch (kv) {
     MEGA_CASE(1)
     MEGA_CASE(2)
@@ -591,9 +680,9 @@ cudaError_t launch_step_mega(const StencilView<T>& SV, const T* x, T* V, long lo
 
 template cudaError_t launch_step_mega<float>(const StencilView<float>&, const float*, float*, long long,
                                              long long, int, float*, StateView<float>, WsView, int,
-                                             cudaStream_t, const float*, float*);
+                                             cudaStream_t, const float*, float*, const MegaX<float>*);
 template cudaError_t launch_step_mega<double>(const StencilView<double>&, const double*, double*, long long,
                                               long long, int, double*, StateView<double>, WsView, int,
-                                              cudaStream_t, const double*, double*);
+                                              cudaStream_t, const double*, double*, const MegaX<double>*);
 
 }  // namespace mpg

@@ -41,7 +41,8 @@ __all__ = ["RowPartition", "plane_partition", "Collectives", "HostStagedCollecti
 PH = {name: i for i, name in enumerate(
     ["BNORM", "POST_BNORM", "RESID", "POST_RESID", "START", "POST_START", "START_SCALE",
      "SPMV_DOT", "POST_DOT1", "UPDATE_DOT", "POST_DOT2", "UPDATE_NORM", "POST_NORM", "SCALE",
-     "FINISH"])}
+     "FINISH", "STEP"])}
+MEGA_MAX_K = 56   # csrc/state.cuh kMegaMaxK: the persistent step covers k <= 56 basis vectors
 
 
 def plane_partition(n_planes: int, world: int) -> list[tuple[int, int]]:
@@ -181,7 +182,7 @@ class DistributedStencilSolver:
 
     def __init__(self, spec, part: RowPartition, mode: str, m: int, rtol: float,
                  collectives, precision: Precision = FP64, b_local=None, use_graph: bool = True,
-                 peer_halo: bool = False, group=None):
+                 peer_halo: bool = False, group=None, persistent: bool = False):
         from .gen import generate_rows
         if mode not in ("ir", "restarted"):
             raise ValueError("mode must be 'ir' or 'restarted'")
@@ -249,6 +250,12 @@ class DistributedStencilSolver:
         d.dia = ptr(self._dia[self.prec])
         d.dia64 = ptr(self._dia[FP64]) if self.mode == _lib.MODE_IR else None
         d.dist, d.row0, d.halo = 1, part.row0, part.halo
+        # distributed persistent step: one cooperative kernel per Arnoldi step,
+        # its three cross-rank sums over peer-memory exchange boxes (needs the
+        # peer halo across ranks, and every step inside the kernel's k range)
+        self.persistent = bool(persistent) and m <= MEGA_MAX_K
+        if self.persistent and part.world > 1:
+            peer_halo = True
         self.peer = bool(peer_halo) and part.world > 1
         if self.peer:
             try:
@@ -260,9 +267,41 @@ class DistributedStencilSolver:
                 self.peer = False
                 d.peer_prev_V = d.peer_next_V = d.halo_flags = None
                 d.peer_prev_flag = d.peer_next_flag = None
+        if self.persistent:
+            try:
+                self._setup_xbox(d, group)
+            except Exception as exc:  # pragma: no cover - depends on the node's IPC/P2P support
+                import warnings
+                warnings.warn(f"exchange boxes unavailable ({exc}); using the phase path", stacklevel=2)
+                self.persistent = False
+                d.xworld = 0
         h = C.c_void_p()
         _lib.call("mpg_solver_create", C.byref(d), C.byref(h))
         self.handle, self.desc = h, d
+
+    def _setup_xbox(self, d, group) -> None:
+        """Allocate this rank's exchange box (the persistent step's mailbox for
+        the three per-step cross-rank sums) and map every rank's box into this
+        process (CUDA IPC over the process group; NVLink peer memory on one
+        node)."""
+        part = self.part
+        self.xbox = torch.zeros(int(_lib.load().mpg_xbox_bytes()), dtype=torch.uint8, device=self.V_buf.device)
+        d.xworld, d.xrank = part.world, part.rank
+        if part.world == 1:
+            d.xbox[0] = ptr(self.xbox)
+            return
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+        infos = [None] * part.world
+        dist.all_gather_object(infos, reduce_tensor(self.xbox)[1], group=group)
+        self._xmaps = []
+        for r in range(part.world):
+            if r == part.rank:
+                d.xbox[r] = ptr(self.xbox)
+            else:
+                t = rebuild_cuda_tensor(*infos[r])
+                self._xmaps.append(t)
+                d.xbox[r] = t.data_ptr()
 
     def _setup_peer_halo(self, d, group) -> None:
         """Map the neighbours' basis buffers and halo flags into this process
@@ -405,6 +444,16 @@ class DistributedStencilSolver:
         self._allreduce(self.red[:2])
         self._ph("POST_START", 0, m_limit)
         self._ph("START_SCALE", 0, m_limit)
+        if self.persistent:
+            # one cooperative kernel per step: SpMV, CGS2, the three cross-rank
+            # sums (in-kernel over the exchange boxes), Givens, scaling, and the
+            # next halo planes stored into the neighbours
+            self._halo(self.V_row(0))
+            for j in range(m_limit):
+                self._ph("STEP", j, m_limit)
+            self._ph("FINISH", 0, m_limit)
+            self._residual()
+            return
         for j in range(m_limit):
             if j == 0 or not self.peer:      # with peer halos SCALE has already written them
                 self._halo(self.V_row(j))
@@ -424,7 +473,8 @@ class DistributedStencilSolver:
 
 # phase -> profile class (DistributedStencilSolver.profile_cycle)
 _PHASE_CLASS = {"SPMV_DOT": "spmv_dot", "UPDATE_DOT": "update_dot", "UPDATE_NORM": "update_norm",
-                "SCALE": "scale", "POST_DOT1": "post", "POST_DOT2": "post", "POST_NORM": "post"}
+                "SCALE": "scale", "POST_DOT1": "post", "POST_DOT2": "post", "POST_NORM": "post",
+                "STEP": "step"}
 
 
 class _CycleProfile:
@@ -451,7 +501,8 @@ class _CycleProfile:
         def nbytes(cls, j):
             k = j + 1
             return {"spmv_dot": (2 + k + 1) * n * s, "update_dot": (k + 2) * n * s,
-                    "update_norm": (k + 2) * n * s, "scale": 2 * n * s}.get(cls, 0)
+                    "update_norm": (k + 2) * n * s, "scale": 2 * n * s,
+                    "step": 2 * n * s + 3 * k * n * s}.get(cls, 0)
         out: dict = {}
         for cls, j, e0, e1 in self.ev:
             ms = e0.elapsed_time(e1)
@@ -511,12 +562,15 @@ def _dist_solve(solver: DistributedStencilSolver, criteria: StopCriteria, ir: bo
 
 
 def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
-                  b_local=None, *, timer=None, use_graph: bool = True, peer_halo: bool = False) -> SolveReport:
+                  b_local=None, *, timer=None, use_graph: bool = True, peer_halo: bool = False,
+                  persistent: bool = False) -> SolveReport:
     """Row-partitioned GMRES-IR (solvers.py:297-384); x returned as this
-    rank's owned block (device tensor)."""
+    rank's owned block (device tensor).  persistent: one cooperative kernel
+    per Arnoldi step with in-kernel cross-rank sums (MPG_PH_STEP)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "ir", criteria.m, criteria.rtol, collectives,
-                                 b_local=b_local, use_graph=use_graph, peer_halo=peer_halo)
+                                 b_local=b_local, use_graph=use_graph, peer_halo=peer_halo,
+                                 persistent=persistent)
     try:
         return _dist_solve(s, criteria, True, timer)
     finally:
@@ -525,12 +579,13 @@ def dist_gmres_ir(spec, part: RowPartition, collectives, criteria: StopCriteria 
 
 def dist_gmres_restarted(spec, part: RowPartition, collectives, criteria: StopCriteria | None = None,
                          precision: Precision = FP64, b_local=None, *, timer=None,
-                         use_graph: bool = True, peer_halo: bool = False) -> SolveReport:
+                         use_graph: bool = True, peer_halo: bool = False,
+                         persistent: bool = False) -> SolveReport:
     """Row-partitioned GMRES(m) in one precision (solvers.py:251-294)."""
     criteria = criteria or StopCriteria()
     s = DistributedStencilSolver(spec, part, "restarted", criteria.m, criteria.rtol, collectives,
                                  precision=precision, b_local=b_local, use_graph=use_graph,
-                                 peer_halo=peer_halo)
+                                 peer_halo=peer_halo, persistent=persistent)
     try:
         return _dist_solve(s, criteria, False, timer)
     finally:

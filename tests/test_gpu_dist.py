@@ -206,3 +206,94 @@ def test_peer_memory_halo_bitwise_equals_collective_halo(world, kind, nx, mode):
     for a, b in zip(res[False], res[True]):
         assert a[1] == b[1] and a[2] == b[2]
         assert np.array_equal(a[3], b[3])
+
+
+# ---------------------------------------------------------------------------
+# distributed persistent step (MPG_PH_STEP): one cooperative kernel per
+# Arnoldi step per rank, the three cross-rank sums done inside the kernel over
+# peer-memory exchange boxes, the next halo planes stored into the neighbours
+
+@pytest.mark.parametrize("kind,nx,mode", [("laplace3d", 24, "ir"), ("laplace3d", 20, "fp64"),
+                                          ("convdiff2d", 60, "ir"), ("laplace2d", 50, "fp32")])
+def test_world1_persistent_step_bitwise_equals_single_gpu_persistent(kind, nx, mode):
+    """At one rank the exchange is a pass-through (the rank's own sums, read
+    back from its box): the distributed persistent step must reproduce the
+    single-GPU persistent step BIT FOR BIT -- iterations, x and history."""
+    kw = {"convection": 30.0} if kind == "convdiff2d" else {}
+    spec = P.StencilSpec(P.StencilKind(kind), nx, **kw)
+    dims = 3 if kind == "laplace3d" else 2
+    part = RowPartition.for_stencil(dims, nx, 1, 0)
+    crit = P.StopCriteria(rtol=1e-10, m=30, max_iters=3000)
+    A = P.generate(spec)
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    pers = P.solvers.step_kernel("persistent")
+    if mode == "ir":
+        with pers:
+            ref = P.gmres_ir(A, b, criteria=crit)
+        rep = dist_gmres_ir(spec, part, NullCollectives(), crit, persistent=True)
+    else:
+        prec = P.FP64 if mode == "fp64" else P.FP32
+        with pers:
+            ref = P.gmres_restarted(A, b, criteria=crit, precision=prec)
+        rep = dist_gmres_restarted(spec, part, NullCollectives(), crit, precision=prec, persistent=True)
+        if prec is P.FP32:
+            rep.x = rep.x.to(torch.float64)
+    assert rep.total_iters == ref.total_iters
+    assert rep.converged == ref.converged
+    assert torch.equal(rep.x, ref.x)
+    assert rep.residual_history == ref.residual_history
+
+
+def _rank_persistent(rank, world, port, kind, nx, mode, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = P.StencilSpec(P.StencilKind(kind), nx)
+        dims = 3 if kind == "laplace3d" else 2
+        part = RowPartition.for_stencil(dims, nx, world, rank)
+        crit = P.StopCriteria(rtol=1e-10, m=30)
+        coll = HostStagedCollectives()
+        if mode == "ir":
+            rep = dist_gmres_ir(spec, part, coll, crit, persistent=True)
+        else:
+            rep = dist_gmres_restarted(spec, part, coll, crit, persistent=True)
+        out.put((rank, part.row0, part.row1, rep.total_iters, rep.converged,
+                 [tuple(e) for e in rep.residual_history], rep.x.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind,nx,mode", [(2, "laplace3d", 16, "ir"), (3, "laplace2d", 40, "fp64")])
+def test_persistent_step_ranks_sharing_one_gpu_match_single_gpu(world, kind, nx, mode):
+    """2 / 3 processes on one GPU (time-sliced), each running the cooperative
+    step kernel on its planes: the in-kernel exchange (peer stores into the
+    exchange boxes, release / acquire sequence numbers) and the in-kernel
+    halo stores must give every rank the same history, and the gathered
+    solution must match the single-GPU solve (parity rule, x within 1e-8)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_persistent, args=(r, world, port, kind, nx, mode, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    spec = P.StencilSpec(P.StencilKind(kind), nx)
+    A = P.generate(spec)
+    b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
+    crit = P.StopCriteria(rtol=1e-10, m=30)
+    ref = P.gmres_ir(A, b, criteria=crit) if mode == "ir" else P.gmres_restarted(A, b, criteria=crit)
+    iters = {r[3] for r in res}
+    hists = {tuple(r[5]) for r in res}
+    assert len(iters) == 1 and len(hists) == 1          # replicated state identical on every rank
+    got = res[0][3]
+    assert all(r[4] for r in res)
+    assert abs(got - ref.total_iters) <= max(1, int(0.02 * ref.total_iters)) or abs(got - ref.total_iters) == 30
+    x = np.concatenate([r[6] for r in res])
+    xr = ref.x.cpu().numpy()
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= 1e-8

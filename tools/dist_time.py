@@ -1,6 +1,6 @@
-"""Time the row-partitioned path at world size 1 over NCCL (graph vs eager)
-against the fused single-GPU solve at cfg2 (overhead of the distributed
-phases: raw-sum kernels, post kernels, allreduces)."""
+"""Time the row-partitioned path at world size 1 over NCCL -- the phase path
+(graph vs eager) and the distributed persistent step (graph) -- against the
+fused single-GPU solve at cfg2 (overhead of the distributed machinery)."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -17,15 +17,16 @@ spec = P.StencilSpec(P.StencilKind.LAPLACE3D, nx)
 crit = P.StopCriteria(rtol=1e-10, m=50)
 part = RowPartition.for_stencil(3, nx, 1, 0)
 out = {}
-for ug in (True, False):
-    s = DistributedStencilSolver(spec, part, "ir", 50, 1e-10, Collectives(), use_graph=ug)
+for ug, pers in ((True, False), (False, False), (True, True)):
+    s = DistributedStencilSolver(spec, part, "ir", 50, 1e-10, Collectives(), use_graph=ug, persistent=pers)
     def solve():
         s.x_buf.zero_()
         return _dist_solve(s, crit, True, None)
     solve()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); rep = solve(); e1.record(); e1.synchronize()
-    out["dist_graph" if ug else "dist_eager"] = (round(e0.elapsed_time(e1) / 1e3, 4), rep.total_iters)
+    key = "dist_persistent_graph" if pers else ("dist_graph" if ug else "dist_eager")
+    out[key] = (round(e0.elapsed_time(e1) / 1e3, 4), rep.total_iters)
     s.close()
 A = P.generate(spec)
 b = torch.ones(A.n_rows, dtype=torch.float64, device="cuda")
