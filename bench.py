@@ -421,7 +421,7 @@ def cfg5_segment_single() -> dict:
     return out
 
 
-def cfg5_segment_dist(world: int, rank: int, coll, peer: bool, persistent: bool = True) -> dict:
+def cfg5_segment_dist(world: int, rank: int, coll, peer: bool, persistent="auto") -> dict:
     """BASELINE configs[4] row-partitioned over the ranks: GMRES-IR for a fixed
     two restart cycles of Laplace3D 400^3, s/iteration (max over ranks), the
     profiled cycle's per-phase GB/s and communication share."""
@@ -509,7 +509,7 @@ def dist_arm(args, rank: int, world: int):
     # one cooperative kernel per Arnoldi step with the cross-rank sums done
     # in-kernel over peer memory (MPG_DIST_PERSISTENT=0: the phase path, NCCL
     # allreduces between per-phase kernels)
-    pers = os.environ.get("MPG_DIST_PERSISTENT", "1") != "0"
+    pers = "auto" if os.environ.get("MPG_DIST_PERSISTENT", "1") != "0" else False
     solver = DistributedStencilSolver(spec, part, "ir", M, RTOL, coll, peer_halo=peer, persistent=pers)
 
     def solve():
