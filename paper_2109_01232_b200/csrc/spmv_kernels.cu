@@ -56,6 +56,7 @@ __device__ __forceinline__ void consumers_finalize(const T* part, int nparts, in
 template <typename T>
 struct EpiPlain {
   static constexpr bool kPdl = true;   // the Arnoldi-step SpMV (split K_A)
+  static constexpr bool kOrderFree = true;
   const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
   int kcat = KC_SPMV;
   __device__ void mark() const { kt_mark(kt, kcat); }
@@ -314,6 +315,7 @@ struct EpiDot1Warp {
 template <typename T>
 struct EpiPoly {
   static constexpr bool kPdl = false;
+  static constexpr bool kOrderFree = true;
   const mpg_state_header* kt = nullptr;   // kernel-time stamp target (null: untimed)
   int kcat = KC_SPMV;
   __device__ void mark() const { kt_mark(kt, kcat); }
