@@ -462,12 +462,12 @@ def cfg5_segment_dist(world: int, rank: int, coll, peer: bool, persistent="auto"
 def _traffic(cls: str) -> dict:
     """DRAM bytes per launch of kernel class `cls` from the committed ncu capture
     of one cfg2 IR cycle (tools/traffic_from_ncu.py; L2 flushed per launch)."""
-    path = os.path.join(ROOT, "profiles", "r1_traffic_ir_cycle.json")
+    path = os.path.join(ROOT, "profiles", "r2_traffic_ir_cycle.json")
     try:
         with open(path) as f:
             c = json.load(f)["classes"][cls]
         return {"traffic": round(c["dram_bytes_per_launch"]),
-                "traffic_source": "profiles/r1_traffic_ir_cycle.json (ncu dram__bytes_read+write, "
+                "traffic_source": "profiles/r2_traffic_ir_cycle.json (ncu dram__bytes_read+write, "
                                   "mean over the cycle's launches)"}
     except (OSError, KeyError, ValueError):
         return {"traffic": None}
