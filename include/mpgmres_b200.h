@@ -341,6 +341,11 @@ typedef struct {
 
 /* Bytes of one rank's exchange box for the distributed persistent step. */
 int64_t mpg_xbox_bytes(void);
+/* Let kernels on the current device load / store memory of device `peer`
+ * (cudaDeviceEnablePeerAccess; already-enabled and peer == current are OK).
+ * Needed before the peer-memory halo / exchange-box stores reach an IPC
+ * mapping owned by another GPU.  MPG_EUNSUPPORTED if the pair cannot peer. */
+int mpg_enable_peer(int32_t peer);
 
 /* Phases of one distributed restart cycle.  A phase marked
  * "raw" leaves this rank's partial sums in the state (red[] in the working

@@ -79,6 +79,7 @@ _SIGS = {
     "mpg_workspace_bytes": (_i64, []),
     "mpg_solver_desc_bytes": (_i64, []),
     "mpg_xbox_bytes": (_i64, []),
+    "mpg_enable_peer": (C.c_int, [_i32]),
     "mpg_launch_count": (_i64, []),
     "mpg_spmv": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mpg_residual": (C.c_int, [C.c_int, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

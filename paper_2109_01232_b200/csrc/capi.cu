@@ -21,6 +21,22 @@ const char* mpg_version(void) { return "mpgmres_b200 0.1.0 sm_100a"; }
 int64_t mpg_workspace_bytes(void) { return kWsBytes; }
 int64_t mpg_solver_desc_bytes(void) { return (int64_t)sizeof(mpg_solver_desc); }
 int64_t mpg_xbox_bytes(void) { return kXBoxBytes; }
+int mpg_enable_peer(int32_t peer) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return (int)cudaGetLastError();
+  if (peer == dev) return MPG_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can) {
+    cudaGetLastError();
+    return MPG_EUNSUPPORTED;
+  }
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return MPG_OK;
+  }
+  return (int)e;
+}
 int64_t mpg_launch_count(void) { return g_launches.load(); }
 
 int mpg_spmv(int prec, int64_t n, const int32_t* rp, const int32_t* ci, const void* v,

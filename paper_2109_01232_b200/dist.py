@@ -172,6 +172,17 @@ class NullCollectives:
         return None
 
 
+def _enable_peer(dev: torch.device) -> None:
+    """IPC mappings of another GPU's memory are opened in that GPU's context;
+    our kernels on this GPU store into them, which needs peer access from
+    this device (a no-op when the ranks share a device, as in the tests)."""
+    if dev.index is None or dev.index == torch.cuda.current_device():
+        return
+    rc = _lib.load().mpg_enable_peer(int(dev.index))
+    if rc:
+        raise RuntimeError(f"peer access {torch.cuda.current_device()} -> {dev.index} unavailable (rc {rc})")
+
+
 # ---------------------------------------------------------------------------
 # the per-rank native solver
 
@@ -306,6 +317,7 @@ class DistributedStencilSolver:
                 d.xbox[r] = ptr(self.xbox)
             else:
                 t = rebuild_cuda_tensor(*infos[r])
+                _enable_peer(t.device)
                 self._xmaps.append(t)
                 d.xbox[r] = t.data_ptr()
 
@@ -327,6 +339,7 @@ class DistributedStencilSolver:
         def open_peer(r):
             v = rebuild_cuda_tensor(*infos[r]["V"])
             f = rebuild_cuda_tensor(*infos[r]["flags"])
+            _enable_peer(v.device)
             self._peer_maps += [v, f]
             return v.data_ptr() + infos[r]["o"] * s, f.data_ptr(), infos[r]
         d.halo_flags = ptr(self.halo_flags)
