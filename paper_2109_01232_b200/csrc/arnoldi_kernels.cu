@@ -158,8 +158,13 @@ template <typename T, int KV>
 #ifndef MPG_KCS_MINB
 #define MPG_KCS_MINB 1
 #endif
-#ifndef MPG_KCS_BATCH
-#define MPG_KCS_BATCH 4
+// basis loads in flight per thread in K_CS: fp32 4 (2 / 4 / 8: 3.52 / 3.47 /
+// 3.52 ms per cycle), fp64 8 (cfg2 fp64 cycle: 6.92 -> 6.20 ms)
+#ifndef MPG_KCS_BATCH32
+#define MPG_KCS_BATCH32 4
+#endif
+#ifndef MPG_KCS_BATCH64
+#define MPG_KCS_BATCH64 8
 #endif
 __global__ void __launch_bounds__(kThreads, MPG_KB_MINB) k_update_dot_w(const T* __restrict__ V, long long ldv,
                                                            long long n, int k, T* __restrict__ w,
@@ -679,8 +684,8 @@ __global__ void __launch_bounds__(kThreads, MPG_KCS_MINB) k_update_norm_scale(co
 #pragma unroll
     for (int e = 0; e < VN; ++e) u[e] = T(0);
     int i = 0;
-    // MPG_KCS_BATCH basis loads in flight per thread; u accumulates in i order either way
-    constexpr int B = MPG_KCS_BATCH;
+    // B basis loads in flight per thread; u accumulates in i order either way
+    constexpr int B = sizeof(T) == 8 ? MPG_KCS_BATCH64 : MPG_KCS_BATCH32;
     for (; i + B <= k; i += B) {
       T vb[B][VN];
 #pragma unroll

@@ -521,7 +521,12 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
 #endif
   // (fp32 only: fp64 keeps its leading-edge prefetch loop, 283 vs 340 us at
   // 400^3; and from 4M rows: at 3.4M rows the march measured 15.5 -> 16.6 us)
-  if constexpr (S == 7 && sizeof(T) == 4 && order_free<E>::value && MPG_ST_ZB > 0) {
+// fp64 marches too, from 16M rows, with a one-plane-ahead L2 prefetch of the
+// leading edge (400^3: 283 -> 268 us; at 3.4M rows it measured 20.9 -> 22.7 us)
+#ifndef MPG_ST_ZM64
+#define MPG_ST_ZM64 1
+#endif
+  if constexpr (S == 7 && (sizeof(T) == 4 || MPG_ST_ZM64) && order_free<E>::value && MPG_ST_ZB > 0) {
     // z-marching (3-D, constant coefficients, whole planes): each warp owns a
     // 32*VN-row chunk of a plane and marches it through ZB planes; the
     // z-1 / centre windows of plane z are the centre / z+1 windows loaded for
@@ -529,7 +534,7 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
     // (400^3 SpMV 120 -> 114 us, cfg4 IR + poly(25) 0.162 -> 0.152 s).
     // Every row is computed exactly as stencil_group computes it.
     const long long P = (long long)SV.nx * SV.nx;
-    if (K.on && SV.padded && P % VN == 0 && SV.n % P == 0 && SV.n >= (4LL << 20)) {
+    if (K.on && SV.padded && P % VN == 0 && SV.n % P == 0 && SV.n >= (sizeof(T) == 8 ? (16LL << 20) : (4LL << 20))) {
       constexpr int RB = 32 * VN;
       const long long nch = (P + RB - 1) / RB, nzl = SV.n / P;
       // march length: about one (chunk, z-range) item per resident warp (one
@@ -554,6 +559,7 @@ __device__ __forceinline__ void stencil_loop_vec(const StencilView<T>& SV, const
 #pragma unroll 1
         for (long long z = z0; z < z1; ++z, rz += P) {
           T px[S][VN];
+          if (sizeof(T) == 8 && z + 1 < z1 && (lane & 7) == 0) prefetch_l2(x + rz + 2 * P);   // next leading edge
           vload(x + rz + P, px[6]);
           if (ALN) {
             vload(x + rz - nxl, px[1]);
