@@ -33,6 +33,18 @@ def test_solver_descriptor_layout_matches_binding():
     assert C.sizeof(_lib.StateHeader) == 8 * 4 + 8 * 16
 
 
+def test_header_kernel_time_fields_and_exchange_box():
+    """The state header carries the four kernel-time bins after the distributed
+    raw-sum slot; the exchange box holds 3 x 8 x 72 values plus sequence words."""
+    H = _lib.StateHeader
+    assert H.reserved.offset + 8 == H.ktime_ns.offset
+    assert H.ktime_ns.offset + 4 * 8 == H.kt_mark.offset
+    assert H.kt_mark.offset + 8 == C.sizeof(H)
+    lib = _lib.load()
+    assert lib.mpg_xbox_bytes() >= 3 * 8 * 72 * 8 + 3 * 8 * 4 + 4
+    assert _lib.SolverDesc.xbox.offset + 8 * C.sizeof(C.c_void_p) == C.sizeof(_lib.SolverDesc)
+
+
 def test_state_layout_monotone():
     lib = _lib.load()
     for prec in (0, 1):
