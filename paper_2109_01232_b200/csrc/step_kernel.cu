@@ -83,13 +83,87 @@ __device__ __forceinline__ void group_sync(int grp) {
   asm volatile("bar.sync %0, 256;" ::"r"(grp + 1) : "memory");
 }
 
-// Sum column `col` of the CTA partials in a fixed order (warp-level), all lanes get it.
+// Sum column `col` of the CTA partials in a fixed order (warp-level), all lanes
+// get it: lane l adds partials l, l + 32, ... in turn, then the warp tree.  The
+// (up to 5 per lane at G <= 160) loads are issued together before the adds, so
+// the sums after a grid barrier cost one L2 round trip instead of two (the
+// compiler's remainder-then-unroll-by-4 loop serialised them).
 template <typename T>
 __device__ __forceinline__ T sum_column(const T* part, int col, int G) {
   const int lane = threadIdx.x & 31;
+  const T* pc = part + (size_t)col * kMaxParts;
+  constexpr int NL = 5;
+  T v[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) v[i] = lane + 32 * i < G ? __ldcg(pc + lane + 32 * i) : T(0);
   T s = T(0);
-  for (int p = lane; p < G; p += 32) s += __ldcg(part + (size_t)col * kMaxParts + p);
+#pragma unroll
+  for (int i = 0; i < NL; ++i)
+    if (lane + 32 * i < G) s += v[i];
+  for (int p = lane + 32 * NL; p < G; p += 32) s += __ldcg(pc + p);
   return warp_sum(s);
+}
+
+// Two columns per warp (col0 and col1 when has1), all loads in flight together;
+// each column summed exactly as sum_column sums it.
+template <typename T>
+__device__ __forceinline__ void sum_column2(const T* part, int col0, int col1, bool has1, int G, T& s0, T& s1) {
+  const int lane = threadIdx.x & 31;
+  const T* p0 = part + (size_t)col0 * kMaxParts;
+  const T* p1 = part + (size_t)col1 * kMaxParts;
+  constexpr int NL = 5;
+  T v0[NL], v1[NL];
+#pragma unroll
+  for (int i = 0; i < NL; ++i) {
+    const bool in = lane + 32 * i < G;
+    v0[i] = in ? __ldcg(p0 + lane + 32 * i) : T(0);
+    v1[i] = in && has1 ? __ldcg(p1 + lane + 32 * i) : T(0);
+  }
+  T a = T(0), b = T(0);
+#pragma unroll
+  for (int i = 0; i < NL; ++i)
+    if (lane + 32 * i < G) {
+      a += v0[i];
+      b += v1[i];
+    }
+  for (int p = lane + 32 * NL; p < G; p += 32) {
+    a += __ldcg(p0 + p);
+    if (has1) b += __ldcg(p1 + p);
+  }
+  s0 = warp_sum(a);
+  s1 = warp_sum(b);
+}
+
+// Grid barrier on a monotonic 64-bit arrival counter (the step kernel's own
+// word in the workspace, zero at creation; every launch passes its barriers
+// uniformly, so the counter is a multiple of G at each launch's start): each
+// CTA's arrival is one acq_rel atomic add, whose old value names the barrier's
+// target; the CTAs poll the counter itself.  Against the count + generation
+// barrier (arnoldi_common.cuh) this drops the generation read before the
+// arrival and the last arriver's reset + release after it: two L2 round trips
+// off each barrier's critical path.
+#ifndef MPG_MEGA_MONO
+#define MPG_MEGA_MONO 1
+#endif
+__device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(cnt) : "memory");
+    const unsigned long long G = gridDim.x;
+    const unsigned long long target = old - old % G + G;
+    if (old + 1 != target) {
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+      } while ((long long)(v - target) < 0);
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void mega_barrier(const WsView& ws) {
+  if (MPG_MEGA_MONO) grid_barrier_mono(reinterpret_cast<unsigned long long*>(ws.counter + 16));
+  else grid_barrier(ws.counter, ws.counter + 1);
 }
 
 // Distributed persistent step (DIST, MPG_PH_STEP): the same kernel on one
@@ -325,11 +399,16 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   MEGA_STAMP(2)
-  grid_barrier(ws.counter, ws.counter + 1);                                       // B1
+  mega_barrier(ws);                                       // B1
   MEGA_STAMP(3)
-  for (int c = warp; c < k + 2; c += kMegaWarps) {
-    const T s = sum_column(part, kColDot1 + c, G);
-    if (lane == 0) c1v[c] = s;
+  for (int c = warp; c < k + 2; c += 2 * kMegaWarps) {   // k + 2 <= 2 * 32 columns: one round trip
+    const int c2 = c + kMegaWarps;
+    T s0, s1;
+    sum_column2(part, kColDot1 + c, kColDot1 + c2, c2 < k + 2, G, s0, s1);
+    if (lane == 0) {
+      c1v[c] = s0;
+      if (c2 < k + 2) c1v[c2] = s1;
+    }
   }
   __syncthreads();
   if constexpr (DIST) {
@@ -450,11 +529,16 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   MEGA_STAMP(4)
-  grid_barrier(ws.counter, ws.counter + 1);                                       // B2
+  mega_barrier(ws);                                       // B2
   MEGA_STAMP(5)
-  for (int c = warp; c < k; c += kMegaWarps) {
-    const T s = sum_column(part, kColDot2 + c, G);
-    if (lane == 0) c2v[c] = s;
+  for (int c = warp; c < k; c += 2 * kMegaWarps) {
+    const int c2 = c + kMegaWarps;
+    T s0, s1;
+    sum_column2(part, kColDot2 + c, kColDot2 + c2, c2 < k, G, s0, s1);
+    if (lane == 0) {
+      c2v[c] = s0;
+      if (c2 < k) c2v[c2] = s1;
+    }
   }
   __syncthreads();
   if constexpr (DIST) mega_xsum<T>(X, 1, k, seqv, c2v, sv.h);
@@ -517,7 +601,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (kt0) kt_stamp(sv.h, KC_NORM);                    // B3 + the norm's column sum
   }
   MEGA_STAMP(6)
-  grid_barrier(ws.counter, ws.counter + 1);                                       // B3
+  mega_barrier(ws);                                       // B3
   MEGA_STAMP(7)
   if (warp == 0) {
     const T s = sum_column(part, kColNorm, G);

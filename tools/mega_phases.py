@@ -25,3 +25,14 @@ names = ["start", "P1 SpMV done", "P1b dots done", "B1 released", "P2 done", "B2
 for i, nm in enumerate(names):
     col = t[:, i] - t0
     print(f"{nm:16s} min {col.min() / 1e3:8.1f} us  median {np.median(col) / 1e3:8.1f}  max {col.max() / 1e3:8.1f}")
+if os.environ.get("MPG_PHASE_CTAS"):
+    # which CTAs finish each phase last (skew attribution): rank by phase end relative to its start
+    nblk = -(-A.n_rows // 128)
+    nb = np.array([(nblk - 1 - c) // 148 + 1 for c in range(148)])
+    for i, nm in [(2, "P1b"), (4, "P2"), (6, "P3")]:
+        dur = t[:, i] - t[:, i - 1]
+        order = np.argsort(-dur)[:12]
+        print(f"{nm} slowest CTAs (dur us, nb):", [(int(c), round(dur[c] / 1e3, 1), int(nb[c])) for c in order])
+        print(f"{nm} dur: min {dur.min()/1e3:.1f} med {np.median(dur)/1e3:.1f} max {dur.max()/1e3:.1f}; "
+              f"end spread {(t[:, i].max() - np.median(t[:, i]))/1e3:.1f} us")
+    np.save(os.path.join("gpurun_out", "mega_times.npy"), t)
