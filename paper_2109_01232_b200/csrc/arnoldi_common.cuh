@@ -161,11 +161,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 #ifndef MPG_BAR_SC
 #define MPG_BAR_SC 0
 #endif
+// default: the count + generation pair as one 64-bit word (MPG_BAR_WORD=0:
+// separate words, the generation read before arriving)
+#ifndef MPG_BAR_WORD
+#define MPG_BAR_WORD 1
+#endif
 __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g0 = ld_acquire_u32(gen);
 #if MPG_BAR_SC
+    const unsigned g0 = ld_acquire_u32(gen);
     __threadfence();
     if (atomicAdd(count, 1u) == gridDim.x - 1) {
       atomicExch(count, 0u);
@@ -175,7 +180,25 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
       while (ld_acquire_u32(gen) == g0) __nanosleep(20);
     }
     __threadfence();
+#elif MPG_BAR_WORD
+    // count (low) and generation (high) read as one 64-bit word, so the
+    // generation comes back with the arrival instead of a load before it; the
+    // last arriver zeroes the count and bumps the generation in one add
+    (void)gen;   // == count + 1 (the workspace's counter pair)
+    unsigned long long* wd = reinterpret_cast<unsigned long long*>(count);
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(wd) : "memory");
+    if ((unsigned)old == gridDim.x - 1) {
+      asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(wd), "l"((1ull << 32) - gridDim.x) : "memory");
+    } else {
+      const unsigned gw = (unsigned)(old >> 32);
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(wd) : "memory");
+      } while ((unsigned)(v >> 32) == gw);
+    }
 #else
+    const unsigned g0 = ld_acquire_u32(gen);
     unsigned old;
     // release: this CTA's writes (ordered before by bar.sync) precede the
     // arrival; acquire: the last arriver sees every CTA's writes

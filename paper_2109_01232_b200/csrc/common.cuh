@@ -109,8 +109,25 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
 // Returns true in every thread of the last CTA to arrive.  The counter is
 // reset by the elected CTA so the slot can be reused by the next kernel on
 // the same stream.
+#ifndef MPG_RED_ACQREL
+#define MPG_RED_ACQREL 1
+#endif
+__device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
 __device__ __forceinline__ bool last_cta(unsigned int* counter) {
   __shared__ bool is_last;
+#if MPG_RED_ACQREL
+  // acq_rel election: bar.sync + thread 0's cumulative release publish the
+  // CTA's stores; the elected CTA's acquire + bar.sync order its loads after
+  // every CTA's stores (no SC fences on the tail's critical path)
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atom_add_acqrel_u32(counter) == gridDim.x - 1;
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) *counter = 0u;
+#else
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -122,6 +139,7 @@ __device__ __forceinline__ bool last_cta(unsigned int* counter) {
     __threadfence();
     if (threadIdx.x == 0) *counter = 0u;
   }
+#endif
   return is_last;
 }
 
@@ -150,6 +168,16 @@ __device__ __forceinline__ void finalize_columns(const T* part, int nparts, int 
 // partials in the same fixed way and calls out(c, total).  The order depends
 // only on gridDim.x, so results are reproducible.  gcount[0..ngroups] must be
 // zero on entry and are left zero.  Returns true in the CTA that called out.
+// columns per warp with loads in flight together in grid_reduce_cols' two
+// stages.  fp32: 8 (cfg2 IR four-launch 0.478 -> 0.470 s with the acq_rel
+// elections); fp64: 1 (the batch costs the register-capped K_B spills: cfg2
+// fp64 0.911 at 8 vs 0.908 s at 1; profiles/r2_ab_grid_reduce.log)
+#ifndef MPG_RED_CB32
+#define MPG_RED_CB32 8
+#endif
+#ifndef MPG_RED_CB64
+#define MPG_RED_CB64 1
+#endif
 template <int GS, typename T, typename OutF>
 __device__ __forceinline__ bool grid_reduce_cols(const T* part, int ldp, T* gpart,
                                                  unsigned int* gcount, int ncols, OutF out) {
@@ -158,19 +186,49 @@ __device__ __forceinline__ bool grid_reduce_cols(const T* part, int ldp, T* gpar
   const int g = b / GS, ng = (G + GS - 1) / GS;
   const int gsz = min(GS, G - g * GS);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#if MPG_RED_ACQREL
+  // elections by acq_rel atomics: bar.sync orders the CTA's partial stores
+  // before thread 0's (cumulative) release; its acquire + bar.sync orders the
+  // elected CTA's loads after every group member's stores -- no SC fences
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atom_add_acqrel_u32(&gcount[1 + g]) == (unsigned)(gsz - 1);
+  __syncthreads();
+  if (!s_last) return false;
+#else
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) s_last = atomicAdd(&gcount[1 + g], 1u) == (unsigned)(gsz - 1);
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
+#endif
   // stage 1: this group's gsz <= 32 partials, one lane each, warp per column
-  for (int c = w; c < ncols; c += nw) {
-    T v = l < gsz ? __ldcg(part + (size_t)c * ldp + g * GS + l) : T(0);
+  // (columns c, c + nw, ... of a warp: kRedCB of them with their loads in
+  // flight together, then the same per-column shuffle trees)
+  constexpr int kRedCB = sizeof(T) == 8 ? MPG_RED_CB64 : MPG_RED_CB32;
+  for (int c0 = w; c0 < ncols; c0 += nw * kRedCB) {
+    T v[kRedCB];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (l == 0) gpart[(size_t)c * 64 + g] = v;
+    for (int i = 0; i < kRedCB; ++i) {
+      const int c = c0 + i * nw;
+      v[i] = (c < ncols && l < gsz) ? __ldcg(part + (size_t)c * ldp + g * GS + l) : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < kRedCB; ++i) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+      if (l == 0 && c0 + i * nw < ncols) gpart[(size_t)(c0 + i * nw) * 64 + g] = v[i];
+    }
   }
+#if MPG_RED_ACQREL
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gcount[1 + g] = 0u;
+    s_last = atom_add_acqrel_u32(&gcount[0]) == (unsigned)(ng - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+#else
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -180,14 +238,25 @@ __device__ __forceinline__ bool grid_reduce_cols(const T* part, int ldp, T* gpar
   __syncthreads();
   if (!s_last) return false;
   __threadfence();
+#endif
   // stage 2: ng <= 64 group partials, two per lane in a fixed order
-  for (int c = w; c < ncols; c += nw) {
-    const T* gp = gpart + (size_t)c * 64;
-    T v = l < ng ? __ldcg(gp + l) : T(0);
-    if (l + 32 < ng) v += __ldcg(gp + l + 32);
+  for (int c0 = w; c0 < ncols; c0 += nw * kRedCB) {
+    T a[kRedCB], b2[kRedCB];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (l == 0) out(c, v);
+    for (int i = 0; i < kRedCB; ++i) {
+      const T* gp = gpart + (size_t)(c0 + i * nw) * 64;
+      const bool in = c0 + i * nw < ncols;
+      a[i] = in && l < ng ? __ldcg(gp + l) : T(0);
+      b2[i] = in && l + 32 < ng ? __ldcg(gp + l + 32) : T(0);
+    }
+#pragma unroll
+    for (int i = 0; i < kRedCB; ++i) {
+      T v = a[i];
+      if (l + 32 < ng) v += b2[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (l == 0 && c0 + i * nw < ncols) out(c0 + i * nw, v);
+    }
   }
   if (threadIdx.x == 0) gcount[0] = 0u;
   return true;
