@@ -161,8 +161,13 @@ __device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt) {
   }
   __syncthreads();
 }
+// The counter word (bytes 64 / 72 of the workspace for fp32 / fp64) belongs to
+// the step kernel of one solver, whose row count and precision -- hence G --
+// are fixed for the workspace's lifetime (solvers.py: one workspace per
+// NativeSolve / distributed solver).
+template <typename T>
 __device__ __forceinline__ void mega_barrier(const WsView& ws) {
-  if (MPG_MEGA_MONO) grid_barrier_mono(reinterpret_cast<unsigned long long*>(ws.counter + 16));
+  if (MPG_MEGA_MONO) grid_barrier_mono(reinterpret_cast<unsigned long long*>(ws.counter + (sizeof(T) == 8 ? 18 : 16)));
   else grid_barrier(ws.counter, ws.counter + 1);
 }
 
@@ -399,7 +404,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   MEGA_STAMP(2)
-  mega_barrier(ws);                                       // B1
+  mega_barrier<T>(ws);                                       // B1
   MEGA_STAMP(3)
   for (int c = warp; c < k + 2; c += 2 * kMegaWarps) {   // k + 2 <= 2 * 32 columns: one round trip
     const int c2 = c + kMegaWarps;
@@ -529,7 +534,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     }
   }
   MEGA_STAMP(4)
-  mega_barrier(ws);                                       // B2
+  mega_barrier<T>(ws);                                       // B2
   MEGA_STAMP(5)
   for (int c = warp; c < k; c += 2 * kMegaWarps) {
     const int c2 = c + kMegaWarps;
@@ -601,7 +606,7 @@ k_step_mega(StencilView<T> SV, const T* __restrict__ x, T* V, long long ldv, lon
     if (kt0) kt_stamp(sv.h, KC_NORM);                    // B3 + the norm's column sum
   }
   MEGA_STAMP(6)
-  mega_barrier(ws);                                       // B3
+  mega_barrier<T>(ws);                                       // B3
   MEGA_STAMP(7)
   if (warp == 0) {
     const T s = sum_column(part, kColNorm, G);
