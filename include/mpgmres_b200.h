@@ -278,7 +278,9 @@ typedef struct {
   void* w;        /* Arnoldi work vector */
   void* u;        /* combination / preconditioner output */
   void* state;    /* mpg_state_bytes(prec, m) */
-  void* ws;       /* mpg_workspace_bytes() */
+  void* ws;       /* mpg_workspace_bytes(), zeroed once, owned by this solver
+                     (the persistent step's grid barrier keeps a monotonic
+                     arrival counter in it for this solver's fixed grid) */
   /* right preconditioner */
   int32_t pc_kind;
   int32_t pc_prec;  /* == prec, or MPG_FP32 inside an fp64 solve (cast_apply) */
