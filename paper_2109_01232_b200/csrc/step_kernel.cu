@@ -145,6 +145,9 @@ __device__ __forceinline__ void sum_column2(const T* part, int col0, int col1, b
 #ifndef MPG_MEGA_MONO
 #define MPG_MEGA_MONO 1
 #endif
+#ifndef MPG_MONO_SLEEP
+#define MPG_MONO_SLEEP 0
+#endif
 __device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -154,9 +157,11 @@ __device__ __forceinline__ void grid_barrier_mono(unsigned long long* cnt) {
     const unsigned long long target = old - old % G + G;
     if (old + 1 != target) {
       unsigned long long v;
-      do {
+      while (true) {
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
-      } while ((long long)(v - target) < 0);
+        if ((long long)(v - target) >= 0) break;
+        if (MPG_MONO_SLEEP > 0) __nanosleep(MPG_MONO_SLEEP);   // A/B: back off the counter's L2 line
+      }
     }
   }
   __syncthreads();
